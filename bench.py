@@ -1,0 +1,345 @@
+#!/usr/bin/env python3
+"""Benchmark: batched counting queries on B200 (BASELINE.json metric: count queries/s and
+scanned GB/s vs HBM peak), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Default workload is BASELINE configs[1] (cfg2: n=100 variables, arity U{2..5}, Dirichlet(1)
+marginals, m=1e6 uint8 instances, 10,000 queries of 1..6 variables, joint tables out).
+A step = the whole query batch on one GPU.  N>1 (torchrun, one rank per GPU) shards a
+N x 10,000-query batch across ranks (query sharding, weak scaling: per-GPU work fixed).
+
+value      device-timed (CUDA events on the launch stream), database and query plan
+           resident in HBM; L2 flushed (256 MB write) before every timed step.
+e2e        through the C ABI one-shot call cs_query_batch with HOST buffers: query
+           descriptors in, every N_ijk table out to pinned host memory, per step.
+roofline   k_hist (the dominant kernel): algorithmic bytes = sum over queries of
+           k * m (every query reads its k uint8 columns once) / execute time.
+cpu_baseline  the oracle's C restatement of the reference radix path (port), all host
+           threads, on a bounded sample of the same queries over the same data.
+--impl reference  times that CPU port alone (the reference is pure Python + numba and
+           cannot run on the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "count queries/s"
+UNIT = "queries/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(config)
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period_s: float = 0.01):
+        self.device = device
+        self.period = period_s
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_workload(config: str, world: int, rank: int, nq_override: int | None):
+    from paper_1804_04640_b200 import workloads as W
+
+    if config == "cfg2":
+        nq = nq_override or 10_000
+        w = W.cfg2(nq=nq * world)
+        mine = w.queries[rank * nq:(rank + 1) * nq]
+        return w, mine
+    if config == "cfg1":
+        w = W.cfg1(nq=nq_override or 1000)
+        return w, w.queries
+    if config == "cfg3":
+        w = W.cfg3()
+        qs = w.queries[rank::world]
+        return w, qs
+    raise SystemExit(f"unsupported --config {config}")
+
+
+def cpu_sample_rate(cols_u8, arities, queries, budget_s: float, threads: int):
+    """Oracle port (C radix restatement) on a bounded sample; returns (q/s, n_sampled, seconds)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    # calibrate on a small prefix, then size the sample to ~budget_s
+    probe = queries[: max(threads * 2, 16)]
+    t0 = time.perf_counter()
+    O.radix_tables(cols_u8, arities, probe, nthreads=threads, want_tables=False)
+    dt = time.perf_counter() - t0
+    rate = len(probe) / max(dt, 1e-6)
+    n = int(min(len(queries), max(len(probe), rate * budget_s)))
+    sample = queries[:n]
+    t0 = time.perf_counter()
+    O.radix_tables(cols_u8, arities, sample, nthreads=threads, want_tables=False)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def host_columns(w):
+    """The workload's columns on the host (twin generator; used by the CPU legs only)."""
+    if w.host_db is not None:
+        return w.host_db.columns_u8()
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import gen_twin
+
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m, dtype=np.int64))
+    return np.vstack([cols[v] for v in range(w.n)])
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU port of the reference path, rank 0 only."""
+    if rank != 0:
+        return
+    w, queries = build_workload(args.config, 1, 0, args.nq)
+    cols = host_columns(w)
+    threads = os.cpu_count() or 1
+    rates = []
+    samples = []
+    for i in range(args.warmup + args.steps):
+        rate, n, dt = cpu_sample_rate(cols, w.arities, queries[(i * 97) % max(len(queries) - 1, 1):] + queries,
+                                      args.ref_budget, threads)
+        if i >= args.warmup:
+            rates.append(rate)
+            samples.append(n)
+    v = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * len(queries) / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": {"workload": w.name, "m": w.m, "n": w.n, "queries": len(queries)},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{int(statistics.mean(samples))} queries of {w.name} per step "
+                                   "(oracle/radix_oracle.c, C restatement of radix_query, "
+                                   f"{threads} threads)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_1804_04640_b200 as cs
+    from paper_1804_04640_b200 import _native as N
+    from paper_1804_04640_b200.engine import GpuContext, QueryPlan, encode_queries
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = GpuContext(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    w, queries = build_workload(args.config, world, rank, args.nq)
+    t0 = time.perf_counter()
+    gdb = w.build_device(ctx)
+    ctx.sync()
+    build_s = time.perf_counter() - t0
+
+    want_tables = args.config in ("cfg1", "cfg2")
+    want_ll = args.config in ("cfg1", "cfg3")
+    flags = N.CS_WANT_TABLES if want_tables else 0
+    plan = QueryPlan(gdb, queries, flags)
+    nq = plan.nq
+    tables = torch.empty(max(plan.total_cells, 1), dtype=torch.int32, device="cuda") if want_tables else None
+    ll = torch.empty(nq, dtype=torch.float64, device="cuda") if want_ll else None
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    algo_bytes = float(sum(len(q) for q in queries)) * w.m
+
+    def step():
+        plan.execute(tables=tables, loglik=ll)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i)  # evict the database from L2 before every timed step (untimed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - l0
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms = float(np.mean(ms))
+    if world > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms = float(t.item())
+
+    # e2e through the C ABI with host buffers (pinned), per step
+    off, flat = encode_queries(queries)
+    h_tables = torch.empty(max(plan.total_cells, 1), dtype=torch.int32, pin_memory=True) if want_tables else None
+    h_ll = torch.empty(nq, dtype=torch.float64, pin_memory=True) if want_ll else None
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gdb.query_batch(off, flat, flags, tables=h_tables, loglik=h_ll)
+        dt = (time.perf_counter() - t0) * 1e3
+        if i >= args.warmup:
+            e2e_ms.append(dt)
+    e2e_step = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    h2d = int(off.nbytes + flat.nbytes)
+    d2h = int((plan.total_cells * 4 if want_tables else 0) + (nq * 8 if want_ll else 0))
+
+    total_q = nq * world
+    value = total_q / (step_ms / 1e3)
+    e2e_value = total_q / (e2e_step / 1e3)
+    peak, peak_src = load_peaks()
+    achieved = algo_bytes / (step_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "queries_per_gpu": nq,
+                   "total_cells_per_gpu": int(plan.total_cells), "parallelism": f"query-shard x{world}",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "outputs": ("tables" if want_tables else "") + ("+loglik" if want_ll else ""),
+                   "db_build_seconds": round(build_s, 3)},
+        "scanned_gbs": achieved * world,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": load_traffic(w.name),
+                     "kernel": "k_hist", "peak_source": peak_src,
+                     "note": "algorithmic bytes = sum_q k_q*m per launch; >1 means L2 reuse across queries"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "cs_query_batch, host descriptors in, pinned host tables out"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cols = host_columns(w)
+        threads = os.cpu_count() or 1
+        rate, n, dt = cpu_sample_rate(cols, w.arities, queries, args.ref_budget, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"first {n} of {nq} {w.name} queries ({dt:.1f} s; "
+                                          "oracle/radix_oracle.c radix restatement)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nq", type=int, default=None, help="queries per GPU (default: the config's)")
+    ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of CPU work per sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        args.ref_budget = min(args.ref_budget, 8.0)
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,976 @@
+// countgpu.cu -- host side of libcountgpu.so: the C ABI declared in include/countstream_gpu.h.
+//
+// Planning (which kernel class, replica count, SIMD lane mode and row segmentation each
+// query gets) happens here on the host in C++; the hot loops are the kernels in
+// cs_kernels.cuh.  See DESIGN.md for the kernel classes and their rooflines.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/countstream_gpu.h"
+#include "cs_common.cuh"
+#include "cs_kernels.cuh"
+
+using namespace cs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CS_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      return fail(e_ == cudaErrorMemoryAllocation ? CS_ERR_OOM : CS_ERR_CUDA,          \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,    \
+                  __LINE__);                                                           \
+    }                                                                                  \
+  } while (0)
+
+#define CS_TRY(expr)          \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ != CS_OK) return rc_; \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s && *s ? atoi(s) : dflt;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// handles
+
+struct cs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  int hist_smem = 0;      // dynamic SMEM bytes per K1 CTA
+  int hist_ctas = 0;      // resident K1 CTAs (persistent grid)
+  int64_t launches = 0;
+  // grow-only device scratch for host-bound outputs
+  std::map<int, std::pair<void*, size_t>> scratch;
+  // grow-only pinned staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  int scratch_get(int slot, size_t bytes, void** out) {
+    auto& s = scratch[slot];
+    if (s.second < bytes) {
+      if (s.first) cudaFree(s.first);
+      s.first = nullptr;
+      s.second = 0;
+      size_t want = std::max<size_t>(bytes, 256);
+      CS_CUDA(cudaMalloc(&s.first, want));
+      s.second = want;
+    }
+    *out = s.first;
+    return CS_OK;
+  }
+  int pinned_get(size_t bytes, void** out) {
+    if (pinned_bytes < bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      pinned_bytes = 0;
+      size_t want = std::max<size_t>(bytes, 1 << 20);
+      CS_CUDA(cudaHostAlloc(&pinned, want, cudaHostAllocDefault));
+      pinned_bytes = want;
+    }
+    *out = pinned;
+    return CS_OK;
+  }
+};
+
+struct cs_db {
+  cs_ctx* ctx = nullptr;
+  int32_t n = 0;
+  int64_t m = 0, ld = 0, m_total = 0;
+  uint8_t* cols = nullptr;
+  int32_t* d_arity = nullptr;
+  std::vector<int32_t> arity;
+  // bitmap index
+  uint32_t* planes = nullptr;
+  int64_t words = 0;
+  std::vector<int64_t> plane_off;  // per var, first plane (state 0) offset in words, -1 = none
+};
+
+struct cs_plan {
+  cs_db* db = nullptr;
+  int32_t nq = 0;
+  uint32_t flags = 0;
+  std::vector<QDesc> hq;
+  std::vector<int64_t> cells, table_off;
+  int64_t total_cells = 0;
+  bool needs_global = false;   // some query accumulates into a global table
+  bool needs_zero = false;     // tables must be zeroed before K1
+  std::vector<int32_t> score_list;    // queries scored by K2 after K1 (kind 1/2)
+  std::vector<int32_t> generic_list;  // kind 2 queries
+  int nitems = 0;
+  // device
+  QDesc* d_q = nullptr;
+  WItem* d_items = nullptr;
+  int32_t* d_score_list = nullptr;
+  int32_t* d_generic_list = nullptr;
+  int32_t* d_gvars = nullptr;
+  uint32_t* d_gstride = nullptr;
+  int* d_head = nullptr;
+  uint32_t* d_done = nullptr;
+  uint32_t* d_tables = nullptr;  // plan-owned table buffer when the caller gives none
+  size_t d_tables_cells = 0;
+  const uint32_t* last_dtab = nullptr;  // device tables of the last execute
+};
+
+// ------------------------------------------------------------------------------------------
+// library / context
+
+extern "C" int cs_abi_version(void) { return CS_ABI_VERSION; }
+extern "C" const char* cs_last_error(void) { return g_err.c_str(); }
+
+extern "C" int cs_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  if (count) *count = c;
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
+  if (!out) return fail(CS_ERR_INVALID, "cs_ctx_create: out is NULL");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(CS_ERR_CUDA, "cs_ctx_create: no CUDA device visible");
+  }
+  if (device < 0 || device >= ndev) return fail(CS_ERR_INVALID, "cs_ctx_create: bad device %d", device);
+  CS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(CS_ERR_UNSUPPORTED, "libcountgpu is built for sm_100a; device %d is sm_%d%d",
+                device, prop.major, prop.minor);
+  cs_ctx* c = new cs_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  CS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  // K1 SMEM budget: two 512-thread CTAs per SM by default.
+  int kb = env_int("CS_HIST_SMEM_KB", 104);
+  c->hist_smem = kb * 1024;
+  CS_CUDA(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, c->hist_smem));
+  int per_sm = 0;
+  CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist, CS_HIST_THREADS,
+                                                        c->hist_smem));
+  if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
+  c->hist_ctas = per_sm * c->num_sms;
+  *out = c;
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
+  if (!ctx) return CS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->scratch)
+    if (kv.second.first) cudaFree(kv.second.first);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_set_stream(cs_ctx* ctx, void* stream) {
+  if (!ctx) return fail(CS_ERR_INVALID, "cs_ctx_set_stream: NULL ctx");
+  if (ctx->own_stream && ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  if (stream) {
+    ctx->stream = (cudaStream_t)stream;
+    ctx->own_stream = false;
+  } else {
+    CS_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_sync(cs_ctx* ctx) {
+  if (!ctx) return fail(CS_ERR_INVALID, "cs_ctx_sync: NULL ctx");
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches) {
+  if (!ctx || !launches) return fail(CS_ERR_INVALID, "cs_ctx_launch_count: NULL argument");
+  *launches = ctx->launches;
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_bytes,
+                           int32_t* hist_ctas) {
+  if (!ctx) return fail(CS_ERR_INVALID, "cs_ctx_info: NULL ctx");
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (hist_smem_bytes) *hist_smem_bytes = ctx->hist_smem;
+  if (hist_ctas) *hist_ctas = ctx->hist_ctas;
+  return CS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// database
+
+static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, cs_db** out) {
+  if (!ctx || !out) return fail(CS_ERR_INVALID, "cs_db: NULL argument");
+  if (n < 1 || m < 1)
+    return fail(CS_ERR_INVALID, "database must have at least one variable and one row, got n=%d m=%lld",
+                n, (long long)m);
+  if (!arities) return fail(CS_ERR_INVALID, "cs_db: arities is NULL");
+  for (int i = 0; i < n; ++i) {
+    if (arities[i] < 1) return fail(CS_ERR_INVALID, "every arity must be at least 1 (variable %d)", i);
+    if (arities[i] > CS_MAX_ARITY)
+      return fail(CS_ERR_UNSUPPORTED,
+                  "variable %d has arity %d; the uint8 column layout supports arity <= 256", i,
+                  arities[i]);
+  }
+  CS_CUDA(cudaSetDevice(ctx->device));
+  cs_db* db = new cs_db();
+  db->ctx = ctx;
+  db->n = n;
+  db->m = m;
+  db->m_total = m;
+  db->ld = round_up(m, 256);
+  db->arity.assign(arities, arities + n);
+  db->plane_off.assign(n, -1);
+  cudaError_t e = cudaMalloc(&db->cols, (size_t)n * db->ld);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete db;
+    return fail(CS_ERR_OOM, "cs_db: cannot allocate %lld bytes of columns: %s",
+                (long long)n * db->ld, cudaGetErrorString(e));
+  }
+  CS_CUDA(cudaMalloc(&db->d_arity, sizeof(int32_t) * n));
+  CS_CUDA(cudaMemcpyAsync(db->d_arity, arities, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  // zero padding (and everything: generated DBs fill columns later)
+  CS_CUDA(cudaMemsetAsync(db->cols, 0, (size_t)n * db->ld, ctx->stream));
+  *out = db;
+  return CS_OK;
+}
+
+extern "C" int cs_db_create_empty(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities,
+                                  cs_db** out) {
+  return db_alloc(ctx, n, m, arities, out);
+}
+
+extern "C" int cs_db_create(cs_ctx* ctx, const uint8_t* cols, int32_t n, int64_t m, int64_t ld,
+                            const int32_t* arities, cs_db** out) {
+  if (!cols) return fail(CS_ERR_INVALID, "cs_db_create: cols is NULL");
+  if (ld < m) return fail(CS_ERR_INVALID, "cs_db_create: ld %lld < m %lld", (long long)ld, (long long)m);
+  cs_db* db = nullptr;
+  CS_TRY(db_alloc(ctx, n, m, arities, &db));
+  const cudaMemcpyKind kind = is_device_ptr(cols) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CS_CUDA(cudaMemcpy2DAsync(db->cols, db->ld, cols, ld, m, n, kind, ctx->stream));
+  // validate states against declared arities (Database.__init__, database.py:61-77)
+  unsigned long long* d_bad = nullptr;
+  CS_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long) * n));
+  CS_CUDA(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long) * n, ctx->stream));
+  dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 1024), n);
+  k_check_states<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, m, db->d_arity, d_bad);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> bad(n);
+  CS_CUDA(cudaMemcpyAsync(bad.data(), d_bad, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_bad);
+  for (int i = 0; i < n; ++i) {
+    if (bad[i] != ~0ull) {
+      uint8_t st = 0;
+      cudaMemcpy(&st, db->cols + (int64_t)i * db->ld + (int64_t)bad[i], 1, cudaMemcpyDeviceToHost);
+      int rc = fail(CS_ERR_INVALID, "row %lld: variable %d has state %d, exceeding declared arity %d",
+                    (long long)bad[i] + 1, i, (int)st, db->arity[i]);
+      cudaFree(db->cols);
+      cudaFree(db->d_arity);
+      delete db;
+      return rc;
+    }
+  }
+  *out = db;
+  return CS_OK;
+}
+
+extern "C" int cs_db_generate(cs_db* db, int32_t var, uint64_t seed, int64_t row_offset,
+                              int32_t nparents, const int32_t* parents, const uint32_t* thresholds,
+                              int64_t nthresholds) {
+  if (!db) return fail(CS_ERR_INVALID, "cs_db_generate: NULL db");
+  if (var < 0 || var >= db->n) return fail(CS_ERR_INVALID, "cs_db_generate: bad var %d", var);
+  if (nparents < 0 || nparents > CS_MAXK) return fail(CS_ERR_INVALID, "cs_db_generate: nparents %d", nparents);
+  const int r = db->arity[var];
+  int64_t q = 1;
+  std::vector<const uint8_t*> pcols(nparents);
+  std::vector<uint32_t> pstride(nparents);
+  for (int t = 0; t < nparents; ++t) {
+    const int p = parents[t];
+    if (p < 0 || p >= db->n || p == var) return fail(CS_ERR_INVALID, "cs_db_generate: bad parent %d", p);
+    pcols[t] = db->cols + (int64_t)p * db->ld;
+    pstride[t] = (uint32_t)q;
+    q *= db->arity[p];
+    if (q > (1 << 24)) return fail(CS_ERR_INVALID, "cs_db_generate: parent space too large");
+  }
+  if (nthresholds != q * (r - 1))
+    return fail(CS_ERR_INVALID, "cs_db_generate: expected %lld thresholds, got %lld",
+                (long long)(q * (r - 1)), (long long)nthresholds);
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  // one small device blob: [pcols][pstride][thr]
+  size_t bytes = sizeof(void*) * std::max(nparents, 1) + sizeof(uint32_t) * std::max(nparents, 1) +
+                 sizeof(uint32_t) * std::max<int64_t>(nthresholds, 1);
+  char* blob = nullptr;
+  CS_CUDA(cudaMalloc(&blob, bytes));
+  std::vector<char> h(bytes, 0);
+  size_t o1 = sizeof(void*) * std::max(nparents, 1);
+  size_t o2 = o1 + sizeof(uint32_t) * std::max(nparents, 1);
+  if (nparents) {
+    memcpy(h.data(), pcols.data(), sizeof(void*) * nparents);
+    memcpy(h.data() + o1, pstride.data(), sizeof(uint32_t) * nparents);
+  }
+  if (nthresholds) memcpy(h.data() + o2, thresholds, sizeof(uint32_t) * nthresholds);
+  CS_CUDA(cudaMemcpyAsync(blob, h.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t m = db->m;
+  unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_generate<<<grid, 256, 0, ctx->stream>>>(db->cols + (int64_t)var * db->ld, m, column_key(seed, var),
+                                            row_offset, nparents, (const uint8_t* const*)blob,
+                                            (const uint32_t*)(blob + o1), (const uint32_t*)(blob + o2),
+                                            r - 1);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(blob);
+  return CS_OK;
+}
+
+extern "C" int cs_db_destroy(cs_db* db) {
+  if (!db) return CS_OK;
+  cudaSetDevice(db->ctx->device);
+  cudaStreamSynchronize(db->ctx->stream);
+  if (db->cols) cudaFree(db->cols);
+  if (db->d_arity) cudaFree(db->d_arity);
+  if (db->planes) cudaFree(db->planes);
+  delete db;
+  return CS_OK;
+}
+
+extern "C" int cs_db_shape(cs_db* db, int32_t* n, int64_t* m, int64_t* ld) {
+  if (!db) return fail(CS_ERR_INVALID, "cs_db_shape: NULL db");
+  if (n) *n = db->n;
+  if (m) *m = db->m;
+  if (ld) *ld = db->ld;
+  return CS_OK;
+}
+
+extern "C" int cs_db_columns(cs_db* db, const uint8_t** dev, int64_t* ld) {
+  if (!db) return fail(CS_ERR_INVALID, "cs_db_columns: NULL db");
+  if (dev) *dev = db->cols;
+  if (ld) *ld = db->ld;
+  return CS_OK;
+}
+
+extern "C" int cs_db_download(cs_db* db, int32_t var, int64_t row0, int64_t nrows, uint8_t* host) {
+  if (!db || !host) return fail(CS_ERR_INVALID, "cs_db_download: NULL argument");
+  if (var < 0 || var >= db->n || row0 < 0 || nrows < 0 || row0 + nrows > db->m)
+    return fail(CS_ERR_INVALID, "cs_db_download: out of range");
+  CS_CUDA(cudaSetDevice(db->ctx->device));
+  CS_CUDA(cudaMemcpyAsync(host, db->cols + (int64_t)var * db->ld + row0, nrows, cudaMemcpyDeviceToHost,
+                          db->ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(db->ctx->stream));
+  return CS_OK;
+}
+
+extern "C" int cs_db_set_total_rows(cs_db* db, int64_t m_total) {
+  if (!db || m_total < db->m) return fail(CS_ERR_INVALID, "cs_db_set_total_rows: bad argument");
+  db->m_total = m_total;
+  return CS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// bitmap index
+
+extern "C" int cs_bitmap_build(cs_db* db, int32_t nvars, const int32_t* vars) {
+  if (!db) return fail(CS_ERR_INVALID, "cs_bitmap_build: NULL db");
+  std::vector<int32_t> list;
+  if (!vars || nvars < 0) {
+    list.resize(db->n);
+    std::iota(list.begin(), list.end(), 0);
+  } else {
+    for (int i = 0; i < nvars; ++i) {
+      if (vars[i] < 0 || vars[i] >= db->n) return fail(CS_ERR_INVALID, "cs_bitmap_build: bad var %d", vars[i]);
+      list.push_back(vars[i]);
+    }
+  }
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  // (re)build the whole pool: planes of previously indexed vars are kept by re-adding them
+  for (int v = 0; v < db->n; ++v)
+    if (db->plane_off[v] >= 0 && std::find(list.begin(), list.end(), v) == list.end()) list.push_back(v);
+  std::sort(list.begin(), list.end());
+  list.erase(std::unique(list.begin(), list.end()), list.end());
+  const int64_t words = round_up((db->m + 31) / 32, 32);
+  int64_t total = 0;
+  std::vector<int64_t> off(list.size());
+  for (size_t i = 0; i < list.size(); ++i) {
+    off[i] = total;
+    total += words * db->arity[list[i]];
+  }
+  if (db->planes) {
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(db->planes);
+    db->planes = nullptr;
+  }
+  CS_CUDA(cudaMalloc(&db->planes, sizeof(uint32_t) * std::max<int64_t>(total, 1)));
+  db->words = words;
+  std::fill(db->plane_off.begin(), db->plane_off.end(), -1);
+  for (size_t i = 0; i < list.size(); ++i) db->plane_off[list[i]] = off[i];
+  if (list.empty()) return CS_OK;
+  int32_t* d_vars = nullptr;
+  int64_t* d_off = nullptr;
+  CS_CUDA(cudaMalloc(&d_vars, sizeof(int32_t) * list.size()));
+  CS_CUDA(cudaMalloc(&d_off, sizeof(int64_t) * list.size()));
+  CS_CUDA(cudaMemcpyAsync(d_vars, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * list.size(), cudaMemcpyHostToDevice, ctx->stream));
+  dim3 grid((unsigned)std::min<int64_t>((words + 255) / 256, 4096), (unsigned)list.size());
+  k_bitmap_build<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, db->m, d_vars, db->d_arity, d_off,
+                                                 db->planes, words);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_vars);
+  cudaFree(d_off);
+  return CS_OK;
+}
+
+extern "C" int cs_bitmap_plane(cs_db* db, int32_t var, int32_t state, const uint32_t** dev,
+                               int64_t* words) {
+  if (!db) return fail(CS_ERR_INVALID, "cs_bitmap_plane: NULL db");
+  if (var < 0 || var >= db->n || state < 0 || state >= db->arity[var])
+    return fail(CS_ERR_INVALID, "cs_bitmap_plane: bad (var, state) (%d, %d)", var, state);
+  if (dev) *dev = db->plane_off[var] < 0 ? nullptr : db->planes + db->plane_off[var] + (int64_t)state * db->words;
+  if (words) *words = db->words;
+  return CS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// planning
+
+static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
+                      uint32_t flags, cs_plan** out) {
+  if (!db || !out) return fail(CS_ERR_INVALID, "cs_plan_create: NULL argument");
+  if (nq < 0) return fail(CS_ERR_INVALID, "cs_plan_create: nq < 0");
+  if (nq > 0 && (!var_off || !vars)) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
+  cs_ctx* ctx = db->ctx;
+  const int smem_words = ctx->hist_smem / 4;
+  const int64_t m = db->m;
+  cs_plan* p = new cs_plan();
+  p->db = db;
+  p->nq = nq;
+  p->flags = flags;
+  p->hq.resize(nq);
+  p->cells.resize(nq);
+  p->table_off.resize(nq);
+  std::vector<int32_t> gvars;
+  std::vector<uint32_t> gstride;
+  int64_t total = 0;
+  const int64_t max_dense = (int64_t)env_int("CS_MAX_DENSE_LOG2", 30);
+  for (int q = 0; q < nq; ++q) {
+    const int b = var_off[q], e = var_off[q + 1];
+    const int k = e - b;
+    if (k < 1) {
+      delete p;
+      return fail(CS_ERR_INVALID, "query %d has no target variable", q);
+    }
+    QDesc d;
+    memset(&d, 0, sizeof d);
+    int64_t c = 1;
+    int nbyte = 0;
+    for (int i = 0; i < k; ++i) {
+      const int v = vars[b + i];
+      if (v < 0 || v >= db->n) {
+        delete p;
+        return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
+      }
+      for (int j = 0; j < i; ++j)
+        if (vars[b + j] == v) {
+          delete p;
+          return fail(CS_ERR_INVALID, "query %d repeats variable %d", q, v);
+        }
+      if (i < CS_MAXK) {
+        d.col[i] = db->cols + (int64_t)v * db->ld;
+        d.stride[i] = (uint32_t)c;
+      }
+      c *= db->arity[v];
+      if (c > ((int64_t)1 << max_dense)) {
+        delete p;
+        return fail(CS_ERR_UNSUPPORTED,
+                    "query %d: joint state space exceeds the dense-table limit 2^%lld cells", q,
+                    (long long)max_dense);
+      }
+      if (c <= 256) nbyte = i + 1;
+    }
+    d.k = k;
+    d.cells = (uint32_t)c;
+    d.nbyte = std::max(nbyte, 1);
+    d.mode = c <= 256 ? 0 : (c <= 65536 ? 1 : 2);
+    d.r_target = db->arity[vars[b]];
+    d.table_off = total;
+    if (k > CS_MAXK) {
+      d.kind = 2;
+      d.var_base = (int32_t)gvars.size();
+      int64_t s = 1;
+      for (int i = 0; i < k; ++i) {
+        gvars.push_back(vars[b + i]);
+        gstride.push_back((uint32_t)s);
+        s *= db->arity[vars[b + i]];
+      }
+    } else if (c <= smem_words) {
+      d.kind = 0;
+      int rl = 0;
+      while (rl < 5 && (c << (rl + 1)) <= smem_words) ++rl;
+      d.rlog = rl;
+    } else {
+      d.kind = 1;
+    }
+    p->hq[q] = d;
+    p->cells[q] = c;
+    p->table_off[q] = total;
+    total += c;
+  }
+  p->total_cells = total;
+  // row segmentation: >= 4 work items per resident CTA, segments of 64K..4M rows
+  const int64_t seg_min = 1 << 16, seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
+  const int64_t target_items = 4LL * ctx->hist_ctas;
+  std::vector<WItem> items;
+  std::vector<double> cost;
+  for (int q = 0; q < nq; ++q) {
+    QDesc& d = p->hq[q];
+    if (d.kind == 2) {
+      p->generic_list.push_back(q);
+      p->score_list.push_back(q);
+      p->needs_global = p->needs_zero = true;
+      d.nseg = 1;
+      continue;
+    }
+    int64_t nseg = std::max<int64_t>(1, (m + seg_max - 1) / seg_max);
+    const int64_t want = (target_items + nq - 1) / std::max(nq, 1);
+    nseg = std::max(nseg, std::min<int64_t>(want, (m + seg_min - 1) / seg_min));
+    int64_t L = round_up((m + nseg - 1) / nseg, 256);
+    nseg = (m + L - 1) / L;
+    d.nseg = (int32_t)nseg;
+    if (d.kind == 1) {
+      p->score_list.push_back(q);
+      p->needs_global = p->needs_zero = true;
+    } else if (nseg > 1) {
+      p->needs_global = p->needs_zero = true;
+    }
+    for (int64_t s = 0; s < nseg; ++s) {
+      WItem w;
+      w.q = q;
+      w.seg = (int32_t)s;
+      w.r0 = s * L;
+      w.r1 = std::min(m, (s + 1) * L);
+      items.push_back(w);
+      const double rows = (double)(w.r1 - w.r0);
+      cost.push_back(rows * (1.0 + d.k) + (d.kind == 0 ? (double)(d.cells << d.rlog) * 2.0 : 0.0));
+    }
+  }
+  // longest-processing-time-first order for the persistent CTAs
+  std::vector<int> order(items.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<WItem> sorted(items.size());
+  for (size_t i = 0; i < order.size(); ++i) sorted[i] = items[order[i]];
+  p->nitems = (int)sorted.size();
+  // upload descriptors (one blob through pinned staging)
+  CS_CUDA(cudaSetDevice(ctx->device));
+  const size_t bq = sizeof(QDesc) * std::max(nq, 1);
+  const size_t bi = sizeof(WItem) * std::max<size_t>(sorted.size(), 1);
+  const size_t bs = sizeof(int32_t) * std::max<size_t>(p->score_list.size(), 1);
+  const size_t bg = sizeof(int32_t) * std::max<size_t>(p->generic_list.size(), 1);
+  const size_t bv = sizeof(int32_t) * std::max<size_t>(gvars.size(), 1);
+  const size_t bst = sizeof(uint32_t) * std::max<size_t>(gstride.size(), 1);
+  size_t off = 0;
+  auto place = [&](size_t bytes) {
+    size_t o = off;
+    off = round_up(off + bytes, 256);
+    return o;
+  };
+  const size_t oq = place(bq), oi = place(bi), os = place(bs), og = place(bg), ov = place(bv),
+               ost = place(bst), oh = place(256), od = place(sizeof(uint32_t) * std::max(nq, 1));
+  char* dblob = nullptr;
+  cudaError_t e = cudaMalloc(&dblob, off);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete p;
+    return fail(CS_ERR_OOM, "cs_plan_create: cannot allocate %zu bytes", off);
+  }
+  void* stage = nullptr;
+  CS_TRY(ctx->pinned_get(off, &stage));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer may be in flight
+  char* hs = (char*)stage;
+  memcpy(hs + oq, p->hq.data(), sizeof(QDesc) * nq);
+  memcpy(hs + oi, sorted.data(), sizeof(WItem) * sorted.size());
+  memcpy(hs + os, p->score_list.data(), sizeof(int32_t) * p->score_list.size());
+  memcpy(hs + og, p->generic_list.data(), sizeof(int32_t) * p->generic_list.size());
+  memcpy(hs + ov, gvars.data(), sizeof(int32_t) * gvars.size());
+  memcpy(hs + ost, gstride.data(), sizeof(uint32_t) * gstride.size());
+  CS_CUDA(cudaMemcpyAsync(dblob, hs, oh, cudaMemcpyHostToDevice, ctx->stream));
+  p->d_q = (QDesc*)(dblob + oq);
+  p->d_items = (WItem*)(dblob + oi);
+  p->d_score_list = (int32_t*)(dblob + os);
+  p->d_generic_list = (int32_t*)(dblob + og);
+  p->d_gvars = (int32_t*)(dblob + ov);
+  p->d_gstride = (uint32_t*)(dblob + ost);
+  p->d_head = (int*)(dblob + oh);
+  p->d_done = (uint32_t*)(dblob + od);
+  *out = p;
+  return CS_OK;
+}
+
+extern "C" int cs_plan_create(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
+                              uint32_t flags, cs_plan** out) {
+  int rc = plan_build(db, nq, var_off, vars, flags, out);
+  if (rc == CS_OK) {
+    // the staging copy must land before the caller may reuse the pinned buffer
+    CS_CUDA(cudaStreamSynchronize(db->ctx->stream));
+  }
+  return rc;
+}
+
+extern "C" int cs_plan_info(cs_plan* p, int64_t* cells, int64_t* table_off, int64_t* total_cells) {
+  if (!p) return fail(CS_ERR_INVALID, "cs_plan_info: NULL plan");
+  if (cells) memcpy(cells, p->cells.data(), sizeof(int64_t) * p->nq);
+  if (table_off) memcpy(table_off, p->table_off.data(), sizeof(int64_t) * p->nq);
+  if (total_cells) *total_cells = p->total_cells;
+  return CS_OK;
+}
+
+extern "C" int cs_plan_destroy(cs_plan* p) {
+  if (!p) return CS_OK;
+  cudaSetDevice(p->db->ctx->device);
+  cudaStreamSynchronize(p->db->ctx->stream);
+  if (p->d_q) cudaFree((void*)p->d_q);  // blob base
+  if (p->d_tables) cudaFree(p->d_tables);
+  delete p;
+  return CS_OK;
+}
+
+// output routing: device pointers are written in place; host pointers go through scratch
+struct OutBuf {
+  void* user = nullptr;
+  void* dev = nullptr;
+  size_t bytes = 0;
+  bool host = false;
+};
+
+static int route(cs_ctx* ctx, int slot, void* user, size_t bytes, OutBuf& ob) {
+  ob.user = user;
+  ob.bytes = bytes;
+  if (!user) return CS_OK;
+  if (is_device_ptr(user)) {
+    ob.dev = user;
+    return CS_OK;
+  }
+  ob.host = true;
+  return ctx->scratch_get(slot, bytes, &ob.dev);
+}
+
+static int plan_tables(cs_plan* p, uint32_t* user_tables, OutBuf& tb, uint32_t** dtab) {
+  const size_t bytes = sizeof(uint32_t) * std::max<int64_t>(p->total_cells, 1);
+  *dtab = nullptr;
+  tb = OutBuf();
+  const bool user_dev = user_tables && is_device_ptr(user_tables);
+  if (user_dev) {
+    tb.user = tb.dev = user_tables;
+    tb.bytes = bytes;
+    *dtab = user_tables;
+  } else if (user_tables || (p->flags & F_TABLES) || p->needs_global) {
+    if (p->d_tables_cells < (size_t)std::max<int64_t>(p->total_cells, 1)) {
+      if (p->d_tables) cudaFree(p->d_tables);
+      p->d_tables = nullptr;
+      CS_CUDA(cudaMalloc(&p->d_tables, bytes));
+      p->d_tables_cells = std::max<int64_t>(p->total_cells, 1);
+    }
+    *dtab = p->d_tables;
+    if (user_tables) {
+      tb.user = user_tables;
+      tb.dev = p->d_tables;
+      tb.bytes = sizeof(uint32_t) * p->total_cells;
+      tb.host = true;
+    }
+  }
+  p->last_dtab = *dtab;
+  return CS_OK;
+}
+
+// tables argument of score/compact: NULL = the device tables of the last execute
+static int input_tables(cs_plan* p, const uint32_t* tables, const uint32_t** out) {
+  cs_ctx* ctx = p->db->ctx;
+  if (!tables) {
+    if (!p->last_dtab) return fail(CS_ERR_INVALID, "no device tables: execute with CS_WANT_TABLES first");
+    *out = p->last_dtab;
+    return CS_OK;
+  }
+  if (is_device_ptr(tables)) {
+    *out = tables;
+    return CS_OK;
+  }
+  void* d = nullptr;
+  CS_TRY(ctx->scratch_get(1, sizeof(uint32_t) * std::max<int64_t>(p->total_cells, 1), &d));
+  CS_CUDA(cudaMemcpyAsync(d, tables, sizeof(uint32_t) * p->total_cells, cudaMemcpyHostToDevice, ctx->stream));
+  *out = (const uint32_t*)d;
+  return CS_OK;
+}
+
+static int finish_outputs(cs_ctx* ctx, OutBuf* obs, int nob) {
+  bool any_host = false;
+  for (int i = 0; i < nob; ++i) {
+    if (obs[i].host) {
+      CS_CUDA(cudaMemcpyAsync(obs[i].user, obs[i].dev, obs[i].bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      any_host = true;
+    }
+  }
+  if (any_host) CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, double* mi,
+                               int64_t* nnz) {
+  if (!p) return fail(CS_ERR_INVALID, "cs_plan_execute: NULL plan");
+  cs_db* db = p->db;
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (p->nq == 0) return CS_OK;
+  uint32_t flags = p->flags;
+  if (loglik) flags |= F_LOGLIK;
+  if (mi) flags |= F_MI;
+  if (nnz) flags |= F_NNZ;
+  OutBuf tb, lb, mb, nb;
+  uint32_t* dtab = nullptr;
+  CS_TRY(plan_tables(p, tables, tb, &dtab));
+  const bool partial = (flags & F_PARTIAL) != 0;
+  if (!partial) {
+    CS_TRY(route(ctx, 2, loglik, sizeof(double) * p->nq, lb));
+    CS_TRY(route(ctx, 3, mi, sizeof(double) * p->nq, mb));
+    CS_TRY(route(ctx, 4, nnz, sizeof(int64_t) * p->nq, nb));
+  }
+  if (p->needs_zero && dtab)
+    CS_CUDA(cudaMemsetAsync(dtab, 0, sizeof(uint32_t) * p->total_cells, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(p->d_head, 0, 256, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(p->d_done, 0, sizeof(uint32_t) * p->nq, ctx->stream));
+  const double m_total = (double)db->m_total;
+  if (p->nitems > 0) {
+    const int grid = std::min(ctx->hist_ctas, p->nitems);
+    k_hist<<<grid, CS_HIST_THREADS, ctx->hist_smem, ctx->stream>>>(
+        p->d_q, p->d_items, p->nitems, p->d_head, dtab, p->d_done, (double*)lb.dev, (double*)mb.dev,
+        (int64_t*)nb.dev, flags, m_total);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
+  if (!p->generic_list.empty()) {
+    dim3 grid((unsigned)std::min<int64_t>((db->m + 255) / 256, 1024), (unsigned)p->generic_list.size());
+    k_hist_generic<<<grid, 256, 0, ctx->stream>>>(p->d_q, p->d_generic_list, p->d_gvars, p->d_gstride,
+                                                  db->cols, db->ld, db->m, dtab);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
+  if (!partial && !p->score_list.empty() && (flags & (F_LOGLIK | F_MI | F_NNZ))) {
+    k_score<<<(unsigned)p->score_list.size(), 256, 0, ctx->stream>>>(
+        p->d_q, p->d_score_list, dtab, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev, flags, m_total);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
+  OutBuf obs[4] = {tb, lb, mb, nb};
+  return finish_outputs(ctx, obs, 4);
+}
+
+extern "C" int cs_plan_score(cs_plan* p, const uint32_t* tables, double* loglik, double* mi,
+                             int64_t* nnz) {
+  if (!p) return fail(CS_ERR_INVALID, "cs_plan_score: NULL plan");
+  cs_ctx* ctx = p->db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (p->nq == 0) return CS_OK;
+  uint32_t flags = 0;
+  if (loglik) flags |= F_LOGLIK;
+  if (mi) flags |= F_MI;
+  if (nnz) flags |= F_NNZ;
+  if (!flags) return CS_OK;
+  const uint32_t* dtab = nullptr;
+  CS_TRY(input_tables(p, tables, &dtab));
+  OutBuf lb, mb, nb;
+  CS_TRY(route(ctx, 2, loglik, sizeof(double) * p->nq, lb));
+  CS_TRY(route(ctx, 3, mi, sizeof(double) * p->nq, mb));
+  CS_TRY(route(ctx, 4, nnz, sizeof(int64_t) * p->nq, nb));
+  k_score<<<(unsigned)p->nq, 256, 0, ctx->stream>>>(p->d_q, nullptr, dtab, (double*)lb.dev,
+                                                     (double*)mb.dev, (int64_t*)nb.dev, flags,
+                                                     (double)p->db->m_total);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  OutBuf obs[3] = {lb, mb, nb};
+  return finish_outputs(ctx, obs, 3);
+}
+
+extern "C" int cs_plan_compact(cs_plan* p, const uint32_t* tables, const int64_t* out_off,
+                               int64_t total_nnz, int64_t* cell_idx, int64_t* n_ijk, int64_t* n_ij) {
+  if (!p || !out_off || !cell_idx || !n_ijk || !n_ij)
+    return fail(CS_ERR_INVALID, "cs_plan_compact: NULL argument");
+  cs_ctx* ctx = p->db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (p->nq == 0 || total_nnz == 0) return CS_OK;
+  const uint32_t* dtab = nullptr;
+  CS_TRY(input_tables(p, tables, &dtab));
+  void* d_off = nullptr;
+  CS_TRY(ctx->scratch_get(5, sizeof(int64_t) * p->nq, &d_off));
+  CS_CUDA(cudaMemcpyAsync(d_off, out_off, sizeof(int64_t) * p->nq, cudaMemcpyHostToDevice, ctx->stream));
+  OutBuf a, b, c;
+  CS_TRY(route(ctx, 6, cell_idx, sizeof(int64_t) * total_nnz, a));
+  CS_TRY(route(ctx, 7, n_ijk, sizeof(int64_t) * total_nnz, b));
+  CS_TRY(route(ctx, 8, n_ij, sizeof(int64_t) * total_nnz, c));
+  k_compact<<<(unsigned)p->nq, 256, 0, ctx->stream>>>(p->d_q, dtab, (const int64_t*)d_off,
+                                                       (int64_t*)a.dev, (int64_t*)b.dev, (int64_t*)c.dev);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  OutBuf obs[3] = {a, b, c};
+  CS_TRY(finish_outputs(ctx, obs, 3));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));  // out_off staging reused next call
+  return CS_OK;
+}
+
+extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
+                              uint32_t flags, uint32_t* tables, double* loglik, double* mi,
+                              int64_t* nnz) {
+  cs_plan* p = nullptr;
+  CS_TRY(plan_build(db, nq, var_off, vars, flags, &p));
+  int rc = cs_plan_execute(p, tables, loglik, mi, nnz);
+  cs_plan_destroy(p);
+  return rc;
+}
+
+// ------------------------------------------------------------------------------------------
+// point counts
+
+extern "C" int cs_count_points(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
+                               const int32_t* states, int64_t* counts) {
+  if (!db || !counts) return fail(CS_ERR_INVALID, "cs_count_points: NULL argument");
+  if (nq < 0) return fail(CS_ERR_INVALID, "cs_count_points: nq < 0");
+  if (nq == 0) return CS_OK;
+  if (!var_off || !vars || !states) return fail(CS_ERR_INVALID, "cs_count_points: NULL query arrays");
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  bool all_planes = db->planes != nullptr;
+  for (int q = 0; q < nq; ++q) {
+    for (int j = var_off[q]; j < var_off[q + 1]; ++j) {
+      const int v = vars[j], s = states[j];
+      if (v < 0 || v >= db->n)
+        return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
+      if (s < 0 || s >= db->arity[v])
+        return fail(CS_ERR_INVALID, "state %d out of range for variable %d with arity %d", s, v, db->arity[v]);
+      if (db->plane_off[v] < 0) all_planes = false;
+    }
+  }
+  // queries with no variables count every record (Assignment((), ()) -> m)
+  std::vector<int32_t> qmap;  // non-empty queries
+  std::vector<int32_t> poff(1, 0);
+  std::vector<int64_t> plist;
+  std::vector<int32_t> pvar, pstate;
+  for (int q = 0; q < nq; ++q) {
+    if (var_off[q + 1] == var_off[q]) continue;
+    qmap.push_back(q);
+    for (int j = var_off[q]; j < var_off[q + 1]; ++j) {
+      if (all_planes) plist.push_back(db->plane_off[vars[j]] + (int64_t)states[j] * db->words);
+      pvar.push_back(vars[j]);
+      pstate.push_back(states[j]);
+    }
+    poff.push_back((int32_t)pvar.size());
+  }
+  const int nne = (int)qmap.size();
+  std::vector<int64_t> out(nq, db->m);
+  if (nne > 0) {
+    const size_t b0 = sizeof(int32_t) * poff.size();
+    const size_t b1 = sizeof(int64_t) * std::max<size_t>(plist.size(), 1);
+    const size_t b2 = sizeof(int32_t) * pvar.size();
+    const size_t b3 = sizeof(unsigned long long) * nne;
+    const size_t o1 = round_up(b0, 256), o2 = o1 + round_up(b1, 256), o3 = o2 + round_up(b2, 256),
+                 o4 = o3 + round_up(b2, 256), tot = o4 + round_up(b3, 256);
+    void* blob = nullptr;
+    CS_TRY(ctx->scratch_get(9, tot, &blob));
+    char* d = (char*)blob;
+    CS_CUDA(cudaMemcpyAsync(d, poff.data(), b0, cudaMemcpyHostToDevice, ctx->stream));
+    if (all_planes) CS_CUDA(cudaMemcpyAsync(d + o1, plist.data(), b1, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(d + o2, pvar.data(), b2, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(d + o3, pstate.data(), b2, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemsetAsync(d + o4, 0, b3, ctx->stream));
+    unsigned long long* dc = (unsigned long long*)(d + o4);
+    if (all_planes) {
+      const int64_t wpc = 32768;
+      dim3 grid((unsigned)((db->words + wpc - 1) / wpc), (unsigned)nne);
+      k_points_bitmap<<<grid, 256, 0, ctx->stream>>>((const int32_t*)d, (const int64_t*)(d + o1),
+                                                      db->planes, db->words, wpc, dc);
+    } else {
+      const int64_t rpc = 1 << 20;
+      dim3 grid((unsigned)((db->m + rpc - 1) / rpc), (unsigned)nne);
+      k_points_scan<<<grid, 256, 0, ctx->stream>>>((const int32_t*)d, (const int32_t*)(d + o2),
+                                                    (const int32_t*)(d + o3), db->cols, db->ld, db->m,
+                                                    rpc, dc);
+    }
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> hc(nne);
+    CS_CUDA(cudaMemcpyAsync(hc.data(), dc, b3, cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < nne; ++i) out[qmap[i]] = (int64_t)hc[i];
+  }
+  if (is_device_ptr(counts)) {
+    CS_CUDA(cudaMemcpyAsync(counts, out.data(), sizeof(int64_t) * nq, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    memcpy(counts, out.data(), sizeof(int64_t) * nq);
+  }
+  return CS_OK;
+}
+
+extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* items, int64_t* pairs,
+                                   int64_t* triples) {
+  (void)db; (void)nitems; (void)items; (void)pairs; (void)triples;
+  return fail(CS_ERR_UNSUPPORTED, "cs_itemset_supports: not built yet");
+}

@@ -1,0 +1,67 @@
+// cs_common.cuh -- shared definitions of libcountgpu (B200 / sm_100a counting-query engine).
+//
+// Layout of the device database:
+//   columns : n x ld bytes, variable-major (row i of the reference's int32 (n, m) matrix,
+//             database.py:53, narrowed to uint8), ld = round_up(m, 256) so every column
+//             starts 256-B aligned and every 16-row vector load is aligned and in bounds.
+//             Bytes past m are zero and never counted.
+//   planes  : optional bit planes, one per (variable, state), `words` uint32 per plane,
+//             bit t%32 of word t/32 = record t (reference bitmap.py:29-31 little-endian).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CS_MAXK 8            // variables per query on the templated fast path
+#define CS_HIST_THREADS 512  // threads per histogram CTA
+#define CS_MAX_ARITY 256
+
+namespace cs {
+
+// One counting query as the histogram kernels see it (uniform per CTA).
+struct __align__(16) QDesc {
+  const uint8_t* col[CS_MAXK];  // column base pointers (index digit order: target first)
+  uint32_t stride[CS_MAXK];     // mixed-radix stride of each digit
+  int64_t table_off;            // first cell of this query's table in the packed table buffer
+  uint32_t cells;               // C = prod of arities
+  int32_t k;                    // number of variables (<= CS_MAXK on the fast path)
+  int32_t nbyte;                // leading digits whose cumulative product <= 256 (SIMD byte lanes)
+  int32_t mode;                 // 0: C <= 256 (byte lanes), 1: C <= 65536 (16-bit lanes), 2: 32-bit
+  int32_t rlog;                 // log2 of SMEM replicas (SMEM class)
+  int32_t r_target;             // arity of the target digit
+  int32_t nseg;                 // row segments this query is split into
+  int32_t kind;                 // 0 SMEM class, 1 global-atomic class, 2 generic (k > CS_MAXK)
+  int32_t var_base;             // generic class: offset into the plan's var list
+  int32_t pad_[3];
+};
+
+// One unit of work: rows [r0, r1) of query q.
+struct WItem {
+  int32_t q;
+  int32_t seg;
+  int64_t r0;
+  int64_t r1;
+};
+
+enum : uint32_t {
+  F_TABLES = 0x1u,
+  F_LOGLIK = 0x2u,
+  F_MI = 0x4u,
+  F_NNZ = 0x8u,
+  F_PARTIAL = 0x10u,
+};
+
+// Counter-based generator (twin: oracle/gen_twin.py).  splitmix64 finaliser.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t column_key(uint64_t seed, int32_t var) {
+  return mix64(seed ^ mix64(0x632BE59BD9B4E019ull + (uint64_t)(uint32_t)var));
+}
+__host__ __device__ __forceinline__ uint32_t hash32(uint64_t key, uint64_t row) {
+  return (uint32_t)(mix64(key + row) >> 32);
+}
+
+}  // namespace cs

@@ -1,0 +1,261 @@
+"""Python handles over the C ABI: device context, device database, query plans.
+
+This is the layer the drop-in :class:`~paper_1804_04640_b200.harness.GpuStrategy`
+and the batched workload drivers call.  Arrays passed in may be numpy (host)
+or torch CUDA tensors (device); outputs land wherever the caller's array lives.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_int32, c_int64, c_void_p
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib, ptr
+
+__all__ = ["GpuContext", "GpuDatabase", "QueryPlan", "encode_queries"]
+
+
+def encode_queries(queries: Iterable[Sequence[int]]) -> tuple[np.ndarray, np.ndarray]:
+    """Variable tuples (target first) -> (var_off int32[nq+1], vars int32[sum k])."""
+    qs = [tuple(int(v) for v in q) for q in queries]
+    off = np.zeros(len(qs) + 1, dtype=np.int32)
+    if qs:
+        off[1:] = np.cumsum([len(q) for q in qs])
+    flat = np.fromiter((v for q in qs for v in q), dtype=np.int32, count=int(off[-1]))
+    return off, flat
+
+
+class GpuContext:
+    """One device + one stream (cs_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = c_void_p()
+        check(lib.cs_ctx_create(int(device), byref(h)))
+        self._h = h
+        self.device = int(device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream: int | None) -> None:
+        """Use an external cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+        check(lib.cs_ctx_set_stream(self._h, c_void_p(stream) if stream else None))
+
+    def sync(self) -> None:
+        check(lib.cs_ctx_sync(self._h))
+
+    @property
+    def launches(self) -> int:
+        v = c_int64(0)
+        check(lib.cs_ctx_launch_count(self._h, byref(v)))
+        return int(v.value)
+
+    def info(self) -> dict:
+        a, b, c = c_int32(), c_int32(), c_int32()
+        check(lib.cs_ctx_info(self._h, byref(a), byref(b), byref(c)))
+        return {"num_sms": a.value, "hist_smem_bytes": b.value, "hist_ctas": c.value}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.cs_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GpuDatabase:
+    """Device-resident uint8 column store (cs_db), one instance shard."""
+
+    def __init__(self, ctx: GpuContext, handle, n: int, m: int, arities):
+        self.ctx = ctx
+        self._h = handle
+        self.n = int(n)
+        self.m = int(m)
+        self.arities = np.asarray(arities, dtype=np.int64)
+        self.arities.setflags(write=False)
+        self.m_total = self.m
+
+    @classmethod
+    def from_columns(cls, ctx: GpuContext, cols, arities) -> "GpuDatabase":
+        """cols: (n, m) uint8, numpy or torch CUDA tensor, rows = variables."""
+        if hasattr(cols, "data_ptr"):
+            n, m = cols.shape
+            ld = cols.stride(0)
+            src = cols
+        else:
+            cols = np.ascontiguousarray(cols, dtype=np.uint8)
+            n, m = cols.shape
+            ld = m
+            src = cols
+        ar = np.ascontiguousarray(arities, dtype=np.int32)
+        h = c_void_p()
+        check(lib.cs_db_create(ctx.handle, ptr(src), int(n), int(m), int(ld), ptr(ar), byref(h)))
+        return cls(ctx, h, n, m, ar)
+
+    @classmethod
+    def empty(cls, ctx: GpuContext, n: int, m: int, arities) -> "GpuDatabase":
+        ar = np.ascontiguousarray(arities, dtype=np.int32)
+        h = c_void_p()
+        check(lib.cs_db_create_empty(ctx.handle, int(n), int(m), ptr(ar), byref(h)))
+        return cls(ctx, h, n, m, ar)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def generate(self, var: int, seed: int, thresholds, parents: Sequence[int] = (), row_offset: int = 0):
+        thr = np.ascontiguousarray(thresholds, dtype=np.uint32).ravel()
+        par = np.ascontiguousarray(list(parents), dtype=np.int32)
+        check(
+            lib.cs_db_generate(
+                self._h, int(var), int(seed) & (2**64 - 1), int(row_offset), len(par),
+                ptr(par) if len(par) else None, ptr(thr) if len(thr) else None, len(thr),
+            )
+        )
+
+    def set_total_rows(self, m_total: int) -> None:
+        check(lib.cs_db_set_total_rows(self._h, int(m_total)))
+        self.m_total = int(m_total)
+
+    def download(self, var: int, row0: int = 0, nrows: int | None = None) -> np.ndarray:
+        nrows = self.m - row0 if nrows is None else nrows
+        out = np.empty(nrows, dtype=np.uint8)
+        check(lib.cs_db_download(self._h, int(var), int(row0), int(nrows), ptr(out)))
+        return out
+
+    def columns_ptr(self) -> tuple[int, int]:
+        p = c_void_p()
+        ld = c_int64()
+        check(lib.cs_db_columns(self._h, byref(p), byref(ld)))
+        return int(p.value or 0), int(ld.value)
+
+    def bitmap_build(self, variables: Sequence[int] | None = None) -> None:
+        if variables is None:
+            check(lib.cs_bitmap_build(self._h, -1, None))
+        else:
+            vs = np.ascontiguousarray(list(variables), dtype=np.int32)
+            check(lib.cs_bitmap_build(self._h, len(vs), ptr(vs) if len(vs) else None))
+
+    def bitmap_plane(self, var: int, state: int) -> tuple[int, int]:
+        p = c_void_p()
+        w = c_int64()
+        check(lib.cs_bitmap_plane(self._h, int(var), int(state), byref(p), byref(w)))
+        return int(p.value or 0), int(w.value)
+
+    def plan(self, queries, flags: int = 0) -> "QueryPlan":
+        return QueryPlan(self, queries, flags)
+
+    def query_batch(self, var_off: np.ndarray, vars_: np.ndarray, flags: int = 0, tables=None,
+                    loglik=None, mi=None, nnz=None) -> None:
+        """One-shot cs_query_batch (plan + execute + free) with caller-owned outputs."""
+        check(lib.cs_query_batch(self._h, len(var_off) - 1, ptr(var_off), ptr(vars_), int(flags),
+                                 ptr(tables), ptr(loglik), ptr(mi), ptr(nnz)))
+
+    def count_points(self, assignments) -> np.ndarray:
+        """assignments: iterable of (variables, states) pairs -> int64 counts."""
+        assignments = list(assignments)
+        off = np.zeros(len(assignments) + 1, dtype=np.int32)
+        vs, ss = [], []
+        for i, (v, s) in enumerate(assignments):
+            vs.extend(int(x) for x in v)
+            ss.extend(int(x) for x in s)
+            off[i + 1] = len(vs)
+        va = np.asarray(vs, dtype=np.int32)
+        sa = np.asarray(ss, dtype=np.int32)
+        out = np.zeros(len(assignments), dtype=np.int64)
+        if len(assignments):
+            check(
+                lib.cs_count_points(
+                    self._h, len(assignments), ptr(off), ptr(va) if len(va) else ptr(np.zeros(1, np.int32)),
+                    ptr(sa) if len(sa) else ptr(np.zeros(1, np.int32)), ptr(out),
+                )
+            )
+        return out
+
+    def itemset_supports(self, items: Sequence[int], pairs: bool = True, triples: bool = True):
+        it = np.ascontiguousarray(list(items), dtype=np.int32)
+        k = len(it)
+        pr = np.zeros((k, k), dtype=np.int64) if pairs else None
+        ntri = k * (k - 1) * (k - 2) // 6
+        tr = np.zeros(ntri, dtype=np.int64) if triples else None
+        check(lib.cs_itemset_supports(self._h, k, ptr(it), ptr(pr), ptr(tr)))
+        return pr, tr
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.cs_db_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class QueryPlan:
+    """An uploaded batch of counting queries (cs_plan).
+
+    ``queries`` are variable tuples, target first then parents.  Tables are
+    packed: query q's cells are ``tables[table_off[q] : table_off[q] + cells[q]]``.
+    """
+
+    def __init__(self, db: GpuDatabase, queries, flags: int = 0):
+        self.db = db
+        if isinstance(queries, tuple) and len(queries) == 2 and isinstance(queries[0], np.ndarray):
+            off, flat = queries
+        else:
+            off, flat = encode_queries(queries)
+        self.var_off = np.ascontiguousarray(off, dtype=np.int32)
+        self.vars = np.ascontiguousarray(flat, dtype=np.int32)
+        self.nq = len(self.var_off) - 1
+        self.flags = int(flags)
+        h = c_void_p()
+        vp = ptr(self.vars) if len(self.vars) else ptr(np.zeros(1, np.int32))
+        check(lib.cs_plan_create(db.handle, self.nq, ptr(self.var_off), vp, self.flags, byref(h)))
+        self._h = h
+        self.cells = np.zeros(self.nq, dtype=np.int64)
+        self.table_off = np.zeros(self.nq, dtype=np.int64)
+        tot = c_int64()
+        check(lib.cs_plan_info(h, ptr(self.cells), ptr(self.table_off), byref(tot)))
+        self.total_cells = int(tot.value)
+        self.r_target = db.arities[self.vars[self.var_off[:-1]]] if self.nq else np.zeros(0, np.int64)
+
+    def execute(self, tables=None, loglik=None, mi=None, nnz=None) -> None:
+        check(lib.cs_plan_execute(self._h, ptr(tables), ptr(loglik), ptr(mi), ptr(nnz)))
+
+    def score(self, tables, loglik=None, mi=None, nnz=None) -> None:
+        check(lib.cs_plan_score(self._h, ptr(tables), ptr(loglik), ptr(mi), ptr(nnz)))
+
+    def compact(self, tables, nnz: np.ndarray):
+        """Non-zero cells per query: (offsets[nq+1], cell_idx, n_ijk, n_ij) int64 host arrays."""
+        nnz = np.asarray(nnz, dtype=np.int64)
+        off = np.zeros(self.nq + 1, dtype=np.int64)
+        off[1:] = np.cumsum(nnz)
+        tot = int(off[-1])
+        ci = np.empty(max(tot, 1), dtype=np.int64)
+        a = np.empty(max(tot, 1), dtype=np.int64)
+        b = np.empty(max(tot, 1), dtype=np.int64)
+        if tot:
+            check(lib.cs_plan_compact(self._h, ptr(tables), ptr(off[:-1].copy()), tot, ptr(ci), ptr(a), ptr(b)))
+        return off, ci[:tot], a[:tot], b[:tot]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.cs_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,238 @@
+"""GPU parity: libcountgpu (through the C ABI / drop-in Strategy) vs the pinned oracle.
+
+Counts must be bit-exact; LL / MDL within 1e-9 relative (BASELINE north_star), MI
+within the absolute bound survey 8a derives for its cancellation.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import FIXTURE_X1_GIVEN_X0_X2, case_db, golden_records, rel_close, sweep_db
+
+pytestmark = pytest.mark.gpu
+
+import paper_1804_04640_b200 as cs  # noqa: E402
+from paper_1804_04640_b200 import workloads  # noqa: E402
+from paper_1804_04640_b200.engine import GpuDatabase, QueryPlan  # noqa: E402
+import gen_twin  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return cs.shared_context(0)
+
+
+def _recs(result: set) -> set:
+    return {(r.config, r.k, r.n_ijk, r.n_ij) for r in result}
+
+
+def test_fixture_kats(reference_cases):
+    db = case_db(reference_cases["fixture"])
+    s = cs.GpuStrategy(db)
+    col = cs.RecordCollector()
+    s.query(cs.QuerySpec(1, (0, 2)), col)
+    assert _recs(col.result()) == FIXTURE_X1_GIVEN_X0_X2
+    col = cs.RecordCollector()
+    s.query(cs.QuerySpec(1, (2, 0)), col)
+    assert _recs(col.result()) == FIXTURE_X1_GIVEN_X0_X2
+    assert s.count(cs.Assignment((0, 1, 2), (2, 1, 0))) == 2
+    assert s.count(cs.Assignment((), ())) == 8
+    sink = cs.NullSink()
+    s.query(cs.QuerySpec(1, (0, 2)), sink)
+    assert sink.count == 7
+
+
+@pytest.mark.parametrize("name", ["fixture", "synthetic-ternary", "synthetic-binary",
+                                  "synthetic-mixed-arity", "synthetic-quaternary", "synthetic-wide-binary"])
+def test_reference_cases(reference_cases, name):
+    case = reference_cases[name]
+    db = case_db(case)
+    s = cs.GpuStrategy(db)
+    for q in case["queries"]:
+        qs = cs.QuerySpec(q["target"], tuple(q["parents"]))
+        col = cs.RecordCollector()
+        s.query(qs, col)
+        assert _recs(col.result()) == golden_records(q)
+        ll = cs.LogLikelihood()
+        s.query(qs, ll)
+        assert rel_close(ll.result(), q["loglik"], 1e-9)
+        assert rel_close(cs.mdl_score(db, qs, s), q["mdl"], 1e-9)
+        # unfused stream path (generic aggregator) delivers the same cells
+        class Tally(cs.Aggregator):
+            def __init__(self):
+                self.cells = []
+
+            def accept(self, a, b):
+                self.cells.append((a, b))
+
+            def result(self):
+                return self.cells
+
+        t = Tally()
+        s.query(qs, t)
+        assert sorted(t.result()) == sorted((r[2], r[3]) for r in golden_records(q))
+    res = cs.learn_parents(db, s, max_parents=case["learn"]["maxParents"])
+    for r, want in zip(res, case["learn"]["parentSets"]):
+        assert list(r.parents) == want["parents"]
+        assert rel_close(r.score, want["score"], 1e-9)
+    if "rules" in case:
+        rr = case["rules"]
+        got = cs.mine_rules(db, s, rr["minSupport"], rr["minConfidence"], rr["maxSize"])
+        got = sorted(got, key=lambda r: (list(r.antecedent), r.consequent))
+        assert [(list(r.antecedent), r.consequent) for r in got] == \
+            [(r["antecedent"], r["consequent"]) for r in rr["rules"]]
+        for a, b in zip(got, rr["rules"]):
+            assert rel_close(a.support, b["support"], 1e-12) and rel_close(a.confidence, b["confidence"], 1e-12)
+
+
+def test_random_sweep(random_sweep):
+    for d in random_sweep["dbs"]:
+        db = sweep_db(d)
+        s = cs.GpuStrategy(db)
+        qs = [cs.QuerySpec(q["target"], tuple(q["parents"])) for q in d["queries"]]
+        out = s.query_batch(qs, loglik=True, nnz=True, tables=True)
+        for i, q in enumerate(d["queries"]):
+            want = golden_records(q)
+            c0, c1 = out["table_off"][i], out["table_off"][i] + out["cells"][i]
+            got = O.records_from_table(out["tables"][c0:c1], q["target"], q["parents"], db.arities)
+            assert got == want
+            assert out["nnz"][i] == len(want)
+            assert rel_close(out["loglik"][i], q["loglik"], 1e-9)
+            col = cs.RecordCollector()
+            s.query(qs[i], col)
+            assert _recs(col.result()) == want
+        counts = s.count_batch([cs.Assignment(p["vars"], p["states"]) for p in d["points"]])
+        assert counts.tolist() == [p["count"] for p in d["points"]]
+
+
+def test_point_counts_scan_and_bitmap_paths(random_sweep):
+    for d in random_sweep["dbs"][:20]:
+        db = sweep_db(d)
+        g_scan = cs.GpuStrategy(db, bitmaps=False)
+        g_bits = cs.GpuStrategy(db, bitmaps=True)
+        al = [cs.Assignment(p["vars"], p["states"]) for p in d["points"]]
+        want = [p["count"] for p in d["points"]]
+        assert g_scan.count_batch(al).tolist() == want
+        assert g_bits.count_batch(al).tolist() == want
+
+
+def test_cfg1_bit_exact(ctx, cfg1_golden):
+    g = cfg1_golden
+    w = workloads.cfg1(int(g["seed"]))
+    assert np.array_equal(w.host_db.columns_u8(), g["data"])
+    gdb = w.build_device(ctx)
+    plan = QueryPlan(gdb, [tuple(q) for q in g["queries"]], cs._native.CS_WANT_TABLES)
+    tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+    ll = np.zeros(plan.nq)
+    plan.execute(tables=tabs, loglik=ll)
+    assert np.array_equal(plan.table_off, g["table_off"])
+    assert np.array_equal(tabs, g["tables"])
+    assert np.allclose(ll, g["loglik"], rtol=1e-9, atol=1e-12)
+
+
+def _check_plan_vs_oracle(gdb, cols_u8, arities, queries, rtol=1e-9):
+    plan = QueryPlan(gdb, queries, cs._native.CS_WANT_TABLES)
+    tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+    ll = np.zeros(plan.nq)
+    nnz = np.zeros(plan.nq, dtype=np.int64)
+    plan.execute(tables=tabs, loglik=ll, nnz=nnz)
+    otabs, ooff, oll, onnz = O.radix_tables(cols_u8, arities, queries)
+    assert np.array_equal(plan.table_off, ooff)
+    assert np.array_equal(tabs, otabs)
+    assert np.array_equal(nnz, onnz)
+    assert np.allclose(ll, oll, rtol=rtol, atol=1e-12)
+    return plan, tabs
+
+
+def test_generator_twin_and_cfg2_slice(ctx):
+    w = workloads.cfg2(nq=300, m=200_003)
+    gdb = w.build_device(ctx)
+    rows = np.arange(w.m)
+    cols = gen_twin.generate_workload_columns(w, rows)
+    u8 = np.vstack([cols[v] for v in range(w.n)])
+    for v in range(0, w.n, 7):
+        assert np.array_equal(gdb.download(v), u8[v])
+    _check_plan_vs_oracle(gdb, u8, w.arities, w.queries)
+
+
+def test_cfg3_slice_and_learning(ctx):
+    w = workloads.cfg3(m=50_000, n=12)
+    gdb = w.build_device(ctx)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+    u8 = np.vstack([cols[v] for v in range(w.n)])
+    assert np.array_equal(gdb.download(w.n - 1), u8[w.n - 1])
+    _check_plan_vs_oracle(gdb, u8, w.arities, w.queries[:2000])
+
+
+@pytest.mark.parametrize("env", [{"CS_SEG_MAX_ROWS": "65536"}, {"CS_HIST_SMEM_KB": "8"}])
+def test_multisegment_and_global_classes(env):
+    """Force the multi-segment merge (last-CTA scoring) and the global-atomic class."""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        c = cs.GpuContext(0)
+        w = workloads.cfg2(nq=120, m=400_000, seed=11)
+        gdb = w.build_device(c)
+        cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+        u8 = np.vstack([cols[v] for v in range(w.n)])
+        _check_plan_vs_oracle(gdb, u8, w.arities, w.queries)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_generic_many_variable_queries(ctx):
+    rng = np.random.default_rng(5)
+    n, m = 14, 3001
+    ar = rng.integers(2, 4, size=n)
+    u8 = np.vstack([rng.integers(0, r, m) for r in ar]).astype(np.uint8)
+    gdb = GpuDatabase.from_columns(ctx, u8, ar)
+    qs = [tuple(int(x) for x in rng.choice(n, size=k, replace=False)) for k in (9, 10, 11, 12) for _ in range(3)]
+    _check_plan_vs_oracle(gdb, u8, ar, qs)
+
+
+def test_mi_fused(ctx):
+    w = workloads.cfg2(nq=200, m=100_000, seed=3)
+    gdb = w.build_device(ctx)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+    u8 = np.vstack([cols[v] for v in range(w.n)])
+    qs = [q for q in w.queries if len(q) >= 2][:60]
+    plan = QueryPlan(gdb, qs)
+    mi = np.zeros(plan.nq)
+    ll = np.zeros(plan.nq)
+    plan.execute(loglik=ll, mi=mi)
+    for i, q in enumerate(qs):
+        recs = O.oracle_records(u8, w.arities, q[0], q[1:])
+        want = O.mi_of_records(recs, w.m)
+        ll1 = O.loglik_of_records(recs)
+        ll0 = O.loglik_of_records(O.oracle_records(u8, w.arities, q[0], ()))
+        tol = 1e-9 * (abs(ll1) + abs(ll0)) / w.m
+        assert abs(mi[i] - want) <= tol, (q, mi[i], want)
+
+
+def test_properties_full_size(ctx):
+    """At full cfg2 size: every table sums to m, and marginalising a table over its last
+    parent equals the table of the shorter query (size-independent properties)."""
+    w = workloads.cfg2(nq=400)
+    gdb = w.build_device(ctx)
+    qs = [q for q in w.queries if len(q) >= 2][:200]
+    shorter = [q[:-1] for q in qs]
+    plan = QueryPlan(gdb, qs + shorter, cs._native.CS_WANT_TABLES)
+    tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+    plan.execute(tables=tabs)
+    for i in range(len(qs)):
+        t = tabs[plan.table_off[i]:plan.table_off[i] + plan.cells[i]].astype(np.int64)
+        assert int(t.sum()) == w.m
+        j = i + len(qs)
+        s = tabs[plan.table_off[j]:plan.table_off[j] + plan.cells[j]].astype(np.int64)
+        last = int(w.arities[qs[i][-1]])
+        assert np.array_equal(t.reshape(last, -1).sum(axis=0), s)
