@@ -70,6 +70,9 @@ int cs_ctx_set_stream(cs_ctx* ctx, void* stream);
 int cs_ctx_sync(cs_ctx* ctx);
 /* number of kernels this context has launched so far (bench `gpu_launches`) */
 int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches);
+/* device time (ms, CUDA events on the context stream) of the last K1 histogram launch;
+ * waits for it to finish.  0 if none yet. */
+int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms);
 /* number of SMs / bytes of dynamic smem the histogram kernel uses (diagnostics) */
 int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_bytes, int32_t* hist_ctas);
 

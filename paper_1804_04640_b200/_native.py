@@ -38,6 +38,7 @@ SIGNATURES = [
     ("cs_ctx_set_stream", c_int, [_P, _P]),
     ("cs_ctx_sync", c_int, [_P]),
     ("cs_ctx_launch_count", c_int, [_P, POINTER(c_int64)]),
+    ("cs_ctx_last_kernel_ms", c_int, [_P, POINTER(ctypes.c_float)]),
     ("cs_ctx_info", c_int, [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
     ("cs_db_create", c_int, [_P, _P, c_int32, c_int64, c_int64, _P, POINTER(_P)]),
     ("cs_db_create_empty", c_int, [_P, c_int32, c_int64, _P, POINTER(_P)]),

@@ -78,6 +78,10 @@ struct cs_ctx {
   int num_sms = 0;
   int hist_smem = 0;      // dynamic SMEM bytes per K1 CTA
   int hist_ctas = 0;      // resident K1 CTAs (persistent grid)
+  int hist_threads = 768;
+  int hist_cfg = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the last K1 launch
+  bool ev_valid = false;
   int64_t launches = 0;
   // grow-only device scratch for host-bound outputs
   std::map<int, std::pair<void*, size_t>> scratch;
@@ -136,7 +140,8 @@ struct cs_plan {
   bool needs_zero = false;     // tables must be zeroed before K1
   std::vector<int32_t> score_list;    // queries scored by K2 after K1 (kind 1/2)
   std::vector<int32_t> generic_list;  // kind 2 queries
-  int nitems = 0;
+  int nitems = 0;   // SMEM-class items (k_hist)
+  int ngitems = 0;  // global-class items (k_hist_global), stored after the SMEM items
   // device
   QDesc* d_q = nullptr;
   WItem* d_items = nullptr;
@@ -187,14 +192,37 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   CS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
-  // K1 SMEM budget: two 512-thread CTAs per SM by default.
-  int kb = env_int("CS_HIST_SMEM_KB", 104);
-  c->hist_smem = kb * 1024;
-  CS_CUDA(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, c->hist_smem));
+  // K1 shape (CS_HIST_CFG): "wide" = one 768-thread CTA per SM with ~220 KB SMEM (32
+  // conflict-free replicas up to C = 1760 cells); "widepf" = same + software prefetch for
+  // K <= 4; "full" = one 1024-thread CTA per SM (64 registers); "pair" = two 384-thread CTAs
+  // per SM with 104 KB each.
+  // Default "full": measured fastest on cfg2 (profiles/README.md, round 1).
+  const char* cfg = getenv("CS_HIST_CFG");
+  c->hist_cfg = 2;
+  if (cfg && strcmp(cfg, "wide") == 0) c->hist_cfg = 0;
+  if (cfg && strcmp(cfg, "widepf") == 0) c->hist_cfg = 1;
+  if (cfg && strcmp(cfg, "pair") == 0) c->hist_cfg = 3;
+  static const int kThreads[4] = {768, 768, 1024, 384};
+  c->hist_threads = kThreads[c->hist_cfg];
+  const int smem_cap = (int)prop.sharedMemPerBlockOptin - (int)sizeof(ScoreSmem) - 1024;
+  int kb = env_int("CS_HIST_SMEM_KB", c->hist_cfg == 3 ? 104 : 220);
+  c->hist_smem = std::min(kb * 1024, smem_cap);
+  // the attribute is per function (process-wide): raise it to the device maximum once so
+  // contexts with different budgets can coexist
+  CS_CUDA(cudaFuncSetAttribute(k_hist<768, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+  CS_CUDA(cudaFuncSetAttribute(k_hist<768, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+  CS_CUDA(cudaFuncSetAttribute(k_hist<1024, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+  CS_CUDA(cudaFuncSetAttribute(k_hist<384, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
   int per_sm = 0;
-  CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist, CS_HIST_THREADS,
-                                                        c->hist_smem));
+  switch (c->hist_cfg) {
+    case 0: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<768, 1, false>, 768, c->hist_smem)); break;
+    case 1: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<768, 1, true>, 768, c->hist_smem)); break;
+    case 2: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<1024, 1, false>, 1024, c->hist_smem)); break;
+    default: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<384, 2, false>, 384, c->hist_smem)); break;
+  }
   if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
+  CS_CUDA(cudaEventCreate(&c->ev0));
+  CS_CUDA(cudaEventCreate(&c->ev1));
   c->hist_ctas = per_sm * c->num_sms;
   *out = c;
   return CS_OK;
@@ -207,6 +235,8 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
   for (auto& kv : ctx->scratch)
     if (kv.second.first) cudaFree(kv.second.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return CS_OK;
@@ -237,6 +267,15 @@ extern "C" int cs_ctx_sync(cs_ctx* ctx) {
 extern "C" int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches) {
   if (!ctx || !launches) return fail(CS_ERR_INVALID, "cs_ctx_launch_count: NULL argument");
   *launches = ctx->launches;
+  return CS_OK;
+}
+
+extern "C" int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return fail(CS_ERR_INVALID, "cs_ctx_last_kernel_ms: NULL argument");
+  *ms = 0.f;
+  if (!ctx->ev_valid) return CS_OK;
+  CS_CUDA(cudaEventSynchronize(ctx->ev1));
+  CS_CUDA(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
   return CS_OK;
 }
 
@@ -536,7 +575,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           return fail(CS_ERR_INVALID, "query %d repeats variable %d", q, v);
         }
       if (i < CS_MAXK) {
-        d.col[i] = db->cols + (int64_t)v * db->ld;
+        d.coff[i] = (uint32_t)((int64_t)v * (db->ld / 256));
         d.stride[i] = (uint32_t)c;
       }
       c *= db->arity[v];
@@ -548,10 +587,11 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
       if (c <= 256) nbyte = i + 1;
     }
+    d.base = db->cols;
     d.k = k;
     d.cells = (uint32_t)c;
     d.nbyte = std::max(nbyte, 1);
-    d.mode = c <= 256 ? 0 : (c <= 65536 ? 1 : 2);
+    d.mode = c <= 65536 ? 1 : 2;
     d.r_target = db->arity[vars[b]];
     d.table_off = total;
     if (k > CS_MAXK) {
@@ -565,11 +605,15 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
     } else if (c <= smem_words) {
       d.kind = 0;
+      // replicas: as many as fit (<= 32; R = 32 makes every ATOMS wavefront conflict-free).
+      // When C*R*4 <= 64 KB the byte offsets fit 16-bit SIMD lanes (mode 0, hist_smem_lane16).
       int rl = 0;
       while (rl < 5 && (c << (rl + 1)) <= smem_words) ++rl;
       d.rlog = rl;
+      d.mode = (c << rl) <= 16384 ? 0 : (c <= 65536 ? 1 : 2);
     } else {
       d.kind = 1;
+      d.mode = c <= 65536 ? 1 : 2;
     }
     p->hq[q] = d;
     p->cells[q] = c;
@@ -618,9 +662,15 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   std::vector<int> order(items.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<WItem> sorted(items.size());
-  for (size_t i = 0; i < order.size(); ++i) sorted[i] = items[order[i]];
-  p->nitems = (int)sorted.size();
+  // SMEM-class items first, then global-class items (each list in LPT order)
+  std::vector<WItem> sorted;
+  sorted.reserve(items.size());
+  for (int pass = 0; pass < 2; ++pass)
+    for (size_t i = 0; i < order.size(); ++i)
+      if ((p->hq[items[order[i]].q].kind == 0) == (pass == 0)) sorted.push_back(items[order[i]]);
+  p->nitems = 0;
+  for (const WItem& w : sorted) p->nitems += p->hq[w.q].kind == 0;
+  p->ngitems = (int)sorted.size() - p->nitems;
   // upload descriptors (one blob through pinned staging)
   CS_CUDA(cudaSetDevice(ctx->device));
   const size_t bq = sizeof(QDesc) * std::max(nq, 1);
@@ -799,11 +849,29 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   CS_CUDA(cudaMemsetAsync(p->d_head, 0, 256, ctx->stream));
   CS_CUDA(cudaMemsetAsync(p->d_done, 0, sizeof(uint32_t) * p->nq, ctx->stream));
   const double m_total = (double)db->m_total;
+  if (p->ngitems > 0) {
+    const int grid = std::min(2 * ctx->num_sms, p->ngitems);
+    k_hist_global<<<grid, 512, 0, ctx->stream>>>(p->d_q, p->d_items + p->nitems, p->ngitems,
+                                                 p->d_head + 1, dtab);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
   if (p->nitems > 0) {
     const int grid = std::min(ctx->hist_ctas, p->nitems);
-    k_hist<<<grid, CS_HIST_THREADS, ctx->hist_smem, ctx->stream>>>(
-        p->d_q, p->d_items, p->nitems, p->d_head, dtab, p->d_done, (double*)lb.dev, (double*)mb.dev,
-        (int64_t*)nb.dev, flags, m_total);
+    CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+#define CS_LAUNCH_HIST(T, B, PF)                                                              \
+  k_hist<T, B, PF><<<grid, T, ctx->hist_smem, ctx->stream>>>(                                 \
+      p->d_q, p->d_items, p->nitems, p->d_head, dtab, p->d_done, (double*)lb.dev, (double*)mb.dev, \
+      (int64_t*)nb.dev, flags, m_total)
+    switch (ctx->hist_cfg) {
+      case 0: CS_LAUNCH_HIST(768, 1, false); break;
+      case 1: CS_LAUNCH_HIST(768, 1, true); break;
+      case 2: CS_LAUNCH_HIST(1024, 1, false); break;
+      default: CS_LAUNCH_HIST(384, 2, false); break;
+    }
+#undef CS_LAUNCH_HIST
+    CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->ev_valid = true;
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
   }

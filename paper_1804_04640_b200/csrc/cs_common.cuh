@@ -12,15 +12,15 @@
 #include <cuda_runtime.h>
 
 #define CS_MAXK 8            // variables per query on the templated fast path
-#define CS_HIST_THREADS 512  // threads per histogram CTA
 #define CS_MAX_ARITY 256
 
 namespace cs {
 
 // One counting query as the histogram kernels see it (uniform per CTA).
 struct __align__(16) QDesc {
-  const uint8_t* col[CS_MAXK];  // column base pointers (index digit order: target first)
-  uint32_t stride[CS_MAXK];     // mixed-radix stride of each digit
+  const uint8_t* base;          // database column block
+  uint32_t coff[CS_MAXK];       // column of digit v starts at base + coff[v] * 256
+  uint32_t stride[CS_MAXK];     // mixed-radix stride of each digit (target digit first)
   int64_t table_off;            // first cell of this query's table in the packed table buffer
   uint32_t cells;               // C = prod of arities
   int32_t k;                    // number of variables (<= CS_MAXK on the fast path)
@@ -31,7 +31,7 @@ struct __align__(16) QDesc {
   int32_t nseg;                 // row segments this query is split into
   int32_t kind;                 // 0 SMEM class, 1 global-atomic class, 2 generic (k > CS_MAXK)
   int32_t var_base;             // generic class: offset into the plan's var list
-  int32_t pad_[3];
+  int32_t pad_[1];
 };
 
 // One unit of work: rows [r0, r1) of query q.

@@ -134,56 +134,112 @@ __device__ void score_table(CellFn cell, uint32_t C, int rt, double m_total, uin
 // SMEM=true : ATOMS into lane-replicated table sh[(idx << rlog) | (lane & (R-1))].
 // SMEM=false: RED.ADD into the global table gtab[idx] (tables too large for SMEM).
 
-template <int K, int MODE>
-__device__ __forceinline__ void joint_index16(const uint4 (&w)[K], const uint32_t (&st)[K],
-                                              int nbyte, uint32_t (&idx)[16]) {
+// SMEM class, C * R * 4 <= 65536: the *byte offset* of each row's replica counter,
+// (idx * R + rep) * 4, is built directly in 16-bit SIMD lanes (two rows per 32-bit word):
+// digits with cumulative product <= 256 are combined in byte lanes (one IMAD per digit per
+// 4 rows), split to 16-bit lanes (2 PRMT), remaining digits added per lane pair, and one
+// IMAD per 2 rows applies the x(4R) scale and adds the thread's replica offset.  Each row
+// then costs one extract (LOP3/SHF) and one ATOMS.  Rows past the end of the last vector
+// read zero padding; they are counted into cell 0 of the thread's replica and subtracted
+// once after the loop (no per-row tail predicate).
+
+template <int K>
+__device__ __forceinline__ void load_vec16(uint32_t (&x)[K][4], const uint8_t* p,
+                                           const uint32_t (&co)[K]) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (MODE == 0) {
-      uint32_t acc = word_of(w[0], j);
-#pragma unroll
-      for (int v = 1; v < K; ++v) acc += word_of(w[v], j) * st[v];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) idx[4 * j + b] = (acc >> (8 * b)) & 0xffu;
-    } else if (MODE == 1) {
-      uint32_t a8 = word_of(w[0], j);
-#pragma unroll
-      for (int v = 1; v < K; ++v)
-        if (v < nbyte) a8 += word_of(w[v], j) * st[v];
-      uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-      uint32_t hi = __byte_perm(a8, 0u, 0x4342);
-#pragma unroll
-      for (int v = 1; v < K; ++v) {
-        if (v >= nbyte) {
-          const uint32_t x = word_of(w[v], j);
-          lo += __byte_perm(x, 0u, 0x4140) * st[v];
-          hi += __byte_perm(x, 0u, 0x4342) * st[v];
-        }
-      }
-      idx[4 * j + 0] = lo & 0xffffu;
-      idx[4 * j + 1] = lo >> 16;
-      idx[4 * j + 2] = hi & 0xffffu;
-      idx[4 * j + 3] = hi >> 16;
-    } else {
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        uint32_t acc = 0;
-#pragma unroll
-        for (int v = 0; v < K; ++v) acc += ((word_of(w[v], j) >> (8 * b)) & 0xffu) * st[v];
-        idx[4 * j + b] = acc;
-      }
-    }
+  for (int v = 0; v < K; ++v) {
+    const uint4 t = ldg_stream16(p + ((uint64_t)co[v] << 8));
+    x[v][0] = t.x;
+    x[v][1] = t.y;
+    x[v][2] = t.z;
+    x[v][3] = t.w;
   }
 }
 
+template <int K>
+__device__ __forceinline__ void count_vec16(const uint32_t (&x)[K][4], const uint32_t (&st)[K],
+                                            int nbyte, uint32_t scale, uint32_t rep_pair,
+                                            char* shb) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t a8 = x[0][j];
+#pragma unroll
+    for (int v = 1; v < K; ++v)
+      if (v < nbyte) a8 += x[v][j] * st[v];
+    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K; ++v) {
+      if (v >= nbyte) {
+        lo += __byte_perm(x[v][j], 0u, 0x4140) * st[v];
+        hi += __byte_perm(x[v][j], 0u, 0x4342) * st[v];
+      }
+    }
+    lo = lo * scale + rep_pair;
+    hi = hi * scale + rep_pair;
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
+  }
+}
+
+template <int K, bool PF>
+__device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int64_t r1,
+                                                 uint32_t* sh) {
+  const uint8_t* rowp = q.base + r0;
+  uint32_t co[K], st[K];
+#pragma unroll
+  for (int v = 0; v < K; ++v) {
+    co[v] = q.coff[v];
+    st[v] = q.stride[v];
+  }
+  const int nbyte = q.nbyte;
+  const int rlog = q.rlog;
+  const uint32_t scale = 4u << rlog;
+  const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
+  const uint32_t rep_pair = rep4 | (rep4 << 16);
+  char* shb = reinterpret_cast<char*>(sh);
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + 15) >> 4;
+  const int64_t bd = blockDim.x;
+  int64_t vi = threadIdx.x;
+  if (PF && K <= 4) {
+    // ping-pong: vector i+1's K loads are in flight while vector i is counted
+    uint32_t a[K][4], b[K][4];
+    if (vi < nvec) load_vec16<K>(a, rowp + (vi << 4), co);
+    for (; vi < nvec; vi += 2 * bd) {
+      const bool hb = vi + bd < nvec;
+      if (hb) load_vec16<K>(b, rowp + ((vi + bd) << 4), co);
+      count_vec16<K>(a, st, nbyte, scale, rep_pair, shb);
+      if (!hb) break;
+      if (vi + 2 * bd < nvec) load_vec16<K>(a, rowp + ((vi + 2 * bd) << 4), co);
+      count_vec16<K>(b, st, nbyte, scale, rep_pair, shb);
+    }
+  } else {
+    for (; vi < nvec; vi += bd) {
+      uint32_t a[K][4];
+      load_vec16<K>(a, rowp + (vi << 4), co);
+      count_vec16<K>(a, st, nbyte, scale, rep_pair, shb);
+    }
+  }
+  const int64_t pad = (nvec << 4) - nrows;  // padding rows counted into cell 0
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % bd))
+    atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
+}
+
+// Other classes: scalar 32-bit index per row.
+//   SMEM=true : SMEM tables too large for 16-bit byte offsets (C*R*4 > 65536);
+//   SMEM=false: RED.ADD into the global table (tables too large for SMEM).
+// MODE 1 builds the index in 16-bit lanes (C <= 65536), MODE 2 per row in 32 bits.
 template <int K, int MODE, bool SMEM>
 __device__ __forceinline__ void hist_rows(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
                                           uint32_t* gtab) {
-  const uint8_t* cp[K];
-  uint32_t st[K];
+  const uint8_t* rowp = q.base + r0;
+  uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
-    cp[v] = q.col[v] + r0;
+    co[v] = q.coff[v];
     st[v] = q.stride[v];
   }
   const int nbyte = q.nbyte;
@@ -191,39 +247,69 @@ __device__ __forceinline__ void hist_rows(const QDesc& q, int64_t r0, int64_t r1
   const uint32_t rep = threadIdx.x & ((1u << rlog) - 1u);
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + 15) >> 4;
+  uint32_t* base = SMEM ? sh : gtab;
+  // SMEM: byte address of a row's counter = idx * (4R) + (4 rep + table base): one IMAD
+  const uint32_t scale = 4u << rlog;
+  char* rbase = reinterpret_cast<char*>(sh) + 4u * rep;
   for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
     uint4 w[K];
 #pragma unroll
-    for (int v = 0; v < K; ++v) w[v] = ldg_stream16(cp[v] + (vi << 4));
-    uint32_t idx[16];
-    joint_index16<K, MODE>(w, st, nbyte, idx);
-    const int64_t left = nrows - (vi << 4);
-    if (left >= 16) {
+    for (int v = 0; v < K; ++v) w[v] = ldg_stream16(rowp + (vi << 4) + ((uint64_t)co[v] << 8));
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (SMEM) atomicAdd(sh + ((idx[r] << rlog) | rep), 1u);
-        else atomicAdd(gtab + idx[r], 1u);
-      }
-    } else {
+    for (int j = 0; j < 4; ++j) {
+      uint32_t idx[4];
+      if (MODE == 1) {
+        uint32_t a8 = word_of(w[0], j);
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (r < left) {
-          if (SMEM) atomicAdd(sh + ((idx[r] << rlog) | rep), 1u);
-          else atomicAdd(gtab + idx[r], 1u);
+        for (int v = 1; v < K; ++v)
+          if (v < nbyte) a8 += word_of(w[v], j) * st[v];
+        uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+        uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+        for (int v = 1; v < K; ++v) {
+          if (v >= nbyte) {
+            const uint32_t x = word_of(w[v], j);
+            lo += __byte_perm(x, 0u, 0x4140) * st[v];
+            hi += __byte_perm(x, 0u, 0x4342) * st[v];
+          }
         }
+        idx[0] = lo & 0xffffu;
+        idx[1] = lo >> 16;
+        idx[2] = hi & 0xffffu;
+        idx[3] = hi >> 16;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          uint32_t acc = 0;
+#pragma unroll
+          for (int v = 0; v < K; ++v) acc += __byte_perm(word_of(w[v], j), 0u, 0x4440 + b) * st[v];
+          idx[b] = acc;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (SMEM) atomicAdd(reinterpret_cast<uint32_t*>(rbase + idx[b] * scale), 1u);
+        else atomicAdd(base + idx[b], 1u);
       }
     }
   }
+  const int64_t pad = (nvec << 4) - nrows;
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
+    atomicSub(base + (SMEM ? rep : 0u), (uint32_t)pad);
 }
 
-template <bool SMEM>
+template <bool SMEM, bool PF = false>
 __device__ __forceinline__ void dispatch_rows(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
                                               uint32_t* gtab) {
-#define CS_CASE_K(KK)                                                   \
-  case KK:                                                              \
-    if (q.mode == 0) hist_rows<KK, 0, SMEM>(q, r0, r1, sh, gtab);       \
-    else if (q.mode == 1) hist_rows<KK, 1, SMEM>(q, r0, r1, sh, gtab);  \
-    else hist_rows<KK, 2, SMEM>(q, r0, r1, sh, gtab);                   \
+#define CS_CASE_K(KK)                                                        \
+  case KK:                                                                   \
+    if (SMEM) {                                                              \
+      if (q.mode == 0) hist_smem_lane16<KK, PF>(q, r0, r1, sh);              \
+      else hist_rows<KK, 1, true>(q, r0, r1, sh, gtab);                      \
+    } else {                                                                 \
+      if (q.mode <= 1) hist_rows<KK, 1, false>(q, r0, r1, sh, gtab);         \
+      else hist_rows<KK, 2, false>(q, r0, r1, sh, gtab);                     \
+    }                                                                        \
     break;
   switch (q.k) {
     CS_CASE_K(1)
@@ -244,7 +330,8 @@ __device__ __forceinline__ void dispatch_rows(const QDesc& q, int64_t r0, int64_
 // *head.  kind 0 (SMEM) items finish with the fused epilogue: a single-segment query writes
 // its table and scores straight from SMEM; a multi-segment query adds its partial table into
 // global memory and the last segment to arrive (done[] counter) scores the merged table.
-__global__ void __launch_bounds__(CS_HIST_THREADS, 2)
+template <int THREADS, int MINB, bool PF>
+__global__ void __launch_bounds__(THREADS, MINB)
     k_hist(const QDesc* __restrict__ qd, const WItem* __restrict__ items, int nitems,
            int* __restrict__ head, uint32_t* tables, uint32_t* __restrict__ done, double* ll_out,
            double* mi_out, int64_t* nnz_out, uint32_t flags, double m_total) {
@@ -264,17 +351,13 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 2)
           reinterpret_cast<const int4*>(qd + wi.q)[threadIdx.x];
     __syncthreads();
     const QDesc& q = s_q;
-    if (q.kind != 0) {
-      dispatch_rows<false>(q, wi.r0, wi.r1, nullptr, tables + q.table_off);
-      continue;
-    }
     const int rl = q.rlog;
     const uint32_t R = 1u << rl;
     const uint32_t C = q.cells;
     const uint32_t nw = C << rl;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
     __syncthreads();
-    dispatch_rows<true>(q, wi.r0, wi.r1, sh, nullptr);
+    dispatch_rows<true, PF>(q, wi.r0, wi.r1, sh, nullptr);
     __syncthreads();
     auto cell = [&](uint32_t c) -> uint32_t {
       uint32_t s = 0;
@@ -306,6 +389,28 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 2)
         }
       }
     }
+  }
+}
+
+// K1 global class: tables too large for SMEM; RED.ADD into the (pre-zeroed) global table.
+// Same persistent work-queue scheme as k_hist, no shared memory.
+__global__ void __launch_bounds__(512, 2)
+    k_hist_global(const QDesc* __restrict__ qd, const WItem* __restrict__ items, int nitems,
+                  int* __restrict__ head, uint32_t* tables) {
+  __shared__ QDesc s_q;
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(head, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= nitems) return;
+    const WItem wi = items[it];
+    if (threadIdx.x < (int)(sizeof(QDesc) / 16))
+      reinterpret_cast<int4*>(&s_q)[threadIdx.x] =
+          reinterpret_cast<const int4*>(qd + wi.q)[threadIdx.x];
+    __syncthreads();
+    dispatch_rows<false>(s_q, wi.r0, wi.r1, nullptr, tables + s_q.table_off);
+    __syncthreads();
   }
 }
 

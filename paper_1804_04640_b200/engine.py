@@ -55,6 +55,12 @@ class GpuContext:
         check(lib.cs_ctx_launch_count(self._h, byref(v)))
         return int(v.value)
 
+    def last_kernel_ms(self) -> float:
+        """Device time of the last K1 (k_hist) launch, CUDA events on the context stream."""
+        v = ctypes.c_float(0)
+        check(lib.cs_ctx_last_kernel_ms(self._h, byref(v)))
+        return float(v.value)
+
     def info(self) -> dict:
         a, b, c = c_int32(), c_int32(), c_int32()
         check(lib.cs_ctx_info(self._h, byref(a), byref(b), byref(c)))
