@@ -5,20 +5,26 @@ scanned GB/s vs HBM peak), one JSON line on rank 0.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
 
 Default workload is BASELINE configs[1] (cfg2: n=100 variables, arity U{2..5}, Dirichlet(1)
-marginals, m=1e6 uint8 instances, 10,000 queries of 1..6 variables, joint tables out).
-A step = the whole query batch on one GPU.  N>1 (torchrun, one rank per GPU) shards a
-N x 10,000-query batch across ranks (query sharding, weak scaling: per-GPU work fixed).
+marginals, m=1e6 uint8 instances, 10,000 queries of 1..6 variables, joint tables out) -- the
+config BASELINE's metric is quoted on that fits one GPU.  A step = the whole query batch.
+Other configs (--config cfg1|cfg3|cfg4|cfg5) measure the remaining BASELINE workloads.
 
-value      device-timed (CUDA events on the launch stream), database and query plan
-           resident in HBM; L2 flushed (256 MB write) before every timed step.
-e2e        through the C ABI one-shot call cs_query_batch with HOST buffers: query
-           descriptors in, every N_ijk table out to pinned host memory, per step.
-roofline   k_hist (the dominant kernel): algorithmic bytes = sum over queries of
-           k * m (every query reads its k uint8 columns once) / execute time.
-cpu_baseline  the oracle's C restatement of the reference radix path (port), all host
-           threads, on a bounded sample of the same queries over the same data.
---impl reference  times that CPU port alone (the reference is pure Python + numba and
-           cannot run on the GPU box).
+Multi-GPU (torchrun, one rank per GPU, NCCL):
+  cfg1-cfg4  query sharding: each rank runs its own slice of an N x batch (weak scaling).
+  cfg5       instance sharding: rank g holds rows [g m/N, (g+1) m/N); partial N_ijk tables
+             are summed with an NCCL all-reduce, then LL + MI are scored (strong scaling).
+
+value      units/s over all ranks, device-timed (CUDA events on the launch stream, max over
+           ranks), database + plan resident in HBM; L2 flushed (256 MB write) before every
+           timed step.
+e2e        through the C ABI with HOST buffers each step: query descriptors in, tables /
+           scores / supports out to pinned host memory.
+roofline   the dominant kernel (k_hist, or k_itemsets for cfg4): algorithmic bytes per launch
+            / its device time (library CUDA events, same stream).
+cpu_baseline  the oracle's C restatement of the reference path (port, all host threads) on
+           a bounded sample of the same workload.
+--impl reference  times that CPU port alone (the reference itself is pure Python + numba
+           and cannot travel to the GPU box).
 """
 
 from __future__ import annotations
@@ -53,6 +59,7 @@ def load_peaks() -> tuple[float, str]:
 
 
 def load_traffic(config: str):
+    """dram read+write bytes per launch of the dominant kernel, from the committed ncu capture."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         try:
@@ -66,13 +73,11 @@ class ClockSampler:
     """NVML sampling of SM clock + throttle reasons during the timed region."""
 
     REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+        0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
     }
 
-    def __init__(self, device: int, period_s: float = 0.01):
-        self.device = device
+    def __init__(self, device: int, period_s: float = 0.005):
         self.period = period_s
         self.samples = []
         self.reasons = set()
@@ -96,7 +101,7 @@ class ClockSampler:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
+                    if r & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
@@ -121,85 +126,279 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def build_workload(config: str, world: int, rank: int, nq_override: int | None):
-    from paper_1804_04640_b200 import workloads as W
-
-    if config == "cfg2":
-        nq = nq_override or 10_000
-        w = W.cfg2(nq=nq * world)
-        mine = w.queries[rank * nq:(rank + 1) * nq]
-        return w, mine
-    if config == "cfg1":
-        w = W.cfg1(nq=nq_override or 1000)
-        return w, w.queries
-    if config == "cfg3":
-        w = W.cfg3()
-        qs = w.queries[rank::world]
-        return w, qs
-    raise SystemExit(f"unsupported --config {config}")
-
-
-def cpu_sample_rate(cols_u8, arities, queries, budget_s: float, threads: int):
-    """Oracle port (C radix restatement) on a bounded sample; returns (q/s, n_sampled, seconds)."""
+def _oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle as O
+    import oracle as O  # test infrastructure: only the cpu_baseline / reference legs use it
 
-    # calibrate on a small prefix, then size the sample to ~budget_s
-    probe = queries[: max(threads * 2, 16)]
-    t0 = time.perf_counter()
-    O.radix_tables(cols_u8, arities, probe, nthreads=threads, want_tables=False)
-    dt = time.perf_counter() - t0
-    rate = len(probe) / max(dt, 1e-6)
-    n = int(min(len(queries), max(len(probe), rate * budget_s)))
-    sample = queries[:n]
-    t0 = time.perf_counter()
-    O.radix_tables(cols_u8, arities, sample, nthreads=threads, want_tables=False)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    return O
 
 
-def host_columns(w):
-    """The workload's columns on the host (twin generator; used by the CPU legs only)."""
-    if w.host_db is not None:
-        return w.host_db.columns_u8()
+def _twin():
     sys.path.insert(0, str(ROOT / "oracle"))
     import gen_twin
 
-    cols = gen_twin.generate_workload_columns(w, np.arange(w.m, dtype=np.int64))
-    return np.vstack([cols[v] for v in range(w.n)])
+    return gen_twin
+
+
+def host_columns(w, variables=None, rows=None):
+    """Workload columns on the host for the CPU legs (reference generator or numpy twin)."""
+    if w.host_db is not None:
+        u8 = w.host_db.columns_u8()
+        return u8 if variables is None else u8[list(variables)]
+    rows = np.arange(w.m, dtype=np.int64) if rows is None else rows
+    vs = list(range(w.n)) if variables is None else list(variables)
+    cols = _twin().generate_workload_columns(w, rows, vs)
+    return np.vstack([cols[v] for v in vs])
+
+
+# ---------------------------------------------------------------------------------------------
+# workloads
+
+
+def workload(config: str, world: int, rank: int, nq_override):
+    """(Workload, this rank's query list) for the query configs."""
+    from paper_1804_04640_b200 import workloads as W
+
+    if config == "cfg1":
+        w = W.cfg1(nq=(nq_override or 1000) * world)
+    elif config == "cfg2":
+        w = W.cfg2(nq=(nq_override or 10_000) * world)
+    elif config == "cfg3":
+        w = W.cfg3()
+        if nq_override:
+            w.queries = w.queries[: nq_override * world]
+        return w, w.queries[rank::world]
+    elif config == "cfg5":
+        w = W.cfg5(nq=nq_override or 2_000)
+        return w, w.queries  # instance sharded: every rank runs every query on its rows
+    else:
+        raise SystemExit(f"unsupported --config {config}")
+    per = len(w.queries) // world
+    return w, w.queries[rank * per:(rank + 1) * per]
+
+
+def cpu_rate_queries(w, queries, budget_s, threads, row_limit=None, cols_fn=None):
+    """Oracle port (radix restatement) on a bounded sample of `queries`; q/s scaled to full m.
+
+    cols_fn(vars, nrows) supplies host columns (default: the reference generator / numpy twin);
+    building them is not timed.
+    """
+    O = _oracle()
+    rows = None if row_limit is None or row_limit >= w.m else np.arange(row_limit, dtype=np.int64)
+    m_eff = w.m if rows is None else len(rows)
+
+    def timed(qs):
+        vs = sorted({v for q in qs for v in q})
+        cols = cols_fn(vs, m_eff) if cols_fn else host_columns(w, vs, rows)
+        remap = {v: i for i, v in enumerate(vs)}
+        ar = np.asarray([w.arities[v] for v in vs])
+        t0 = time.perf_counter()
+        O.radix_tables(cols, ar, [tuple(remap[v] for v in q) for q in qs], nthreads=threads,
+                       want_tables=False)
+        return time.perf_counter() - t0
+
+    probe = list(queries[: max(2 * threads, 16)])
+    rate = len(probe) / max(timed(probe), 1e-6)
+    n = int(max(len(probe), rate * budget_s))
+    reps = max(1, -(-n // len(queries)))  # small batches (cfg1) are repeated to fill the budget
+    sample = (list(queries) * reps)[:n]
+    dt = timed(sample)
+    scale = m_eff / w.m  # radix work is linear in m
+    desc = (f"{n} {w.name} queries (of a {len(queries)}-query batch) in {dt:.1f} s "
+            f"(oracle/radix_oracle.c radix restatement, {threads} threads"
+            + (f", on the first {m_eff} rows, rate scaled x{scale:g} to m={w.m}" if rows is not None else "")
+            + ")")
+    return n / dt * scale, desc
+
+
+class QueryRunner:
+    """cfg1/cfg2/cfg3 (query-sharded) and cfg5 (instance-sharded + NCCL merge)."""
+
+    kernel = "k_hist"
+
+    def __init__(self, args, world, rank, local, torch, ctx):
+        from paper_1804_04640_b200 import _native as N
+        from paper_1804_04640_b200.engine import QueryPlan, encode_queries
+
+        self.torch, self.ctx, self.world, self.rank = torch, ctx, world, rank
+        self.config = args.config
+        self.w, self.queries = workload(args.config, world, rank, args.nq)
+        w = self.w
+        self.sharded = args.config == "cfg5" and world > 1
+        t0 = time.perf_counter()
+        if self.sharded:
+            per = (w.m + world - 1) // world
+            self.row0, self.rows = rank * per, min(per, w.m - rank * per)
+            self.gdb = w.build_device(ctx, row_offset=self.row0, m_shard=self.rows)
+        else:
+            self.rows = w.m
+            self.gdb = w.build_device(ctx)
+        ctx.sync()
+        self.build_s = time.perf_counter() - t0
+        self.want_tables = args.config in ("cfg1", "cfg2")
+        self.want_ll = args.config in ("cfg1", "cfg3", "cfg5")
+        self.want_mi = args.config == "cfg5"
+        flags = N.CS_WANT_TABLES if self.want_tables else 0
+        if self.sharded:
+            flags |= N.CS_PARTIAL | N.CS_WANT_TABLES
+        self.flags = flags
+        self.plan = QueryPlan(self.gdb, self.queries, flags)
+        self.units = self.plan.nq
+        dev = "cuda"
+        self.tables = (torch.empty(max(self.plan.total_cells, 1), dtype=torch.int32, device=dev)
+                       if (self.want_tables or self.sharded) else None)
+        self.ll = torch.empty(self.units, dtype=torch.float64, device=dev) if self.want_ll else None
+        self.mi = torch.empty(self.units, dtype=torch.float64, device=dev) if self.want_mi else None
+        self.algo_bytes = float(sum(len(q) for q in self.queries)) * self.rows
+        self.off, self.flat = encode_queries(self.queries)
+        pin = dict(pin_memory=True)
+        self.h_tables = (torch.empty(max(self.plan.total_cells, 1), dtype=torch.int32, **pin)
+                         if self.want_tables else None)
+        self.h_ll = torch.empty(self.units, dtype=torch.float64, **pin) if self.want_ll else None
+        self.h_mi = torch.empty(self.units, dtype=torch.float64, **pin) if self.want_mi else None
+        self.h2d = int(self.off.nbytes + self.flat.nbytes)
+        self.d2h = int((self.plan.total_cells * 4 if self.want_tables else 0)
+                       + self.units * 8 * (int(self.want_ll) + int(self.want_mi)))
+        self.scaling = "strong" if self.sharded else "weak"
+        self.parallelism = (f"instance-shard x{world} + NCCL all-reduce" if self.sharded
+                            else f"query-shard x{world}")
+
+    def step(self):
+        if self.sharded:
+            self.plan.execute(tables=self.tables)
+            self.torch.distributed.all_reduce(self.tables)  # uint32 sum == int32 sum bitwise
+            self.plan.score(self.tables, loglik=self.ll, mi=self.mi)
+        else:
+            self.plan.execute(tables=self.tables, loglik=self.ll, mi=self.mi)
+
+    def e2e_step(self):
+        if self.sharded:
+            self.step()
+            self.h_ll.copy_(self.ll)
+            self.h_mi.copy_(self.mi)
+            self.torch.cuda.synchronize()
+            return
+        self.gdb.query_batch(self.off, self.flat, self.flags, tables=self.h_tables, loglik=self.h_ll,
+                             mi=self.h_mi)
+
+    def describe(self):
+        return {"workload": self.w.name, "n": self.w.n, "m": self.w.m, "queries_per_step": self.units,
+                "total_cells": int(self.plan.total_cells), "parallelism": self.parallelism,
+                "outputs": "+".join(x for x, f in (("tables", self.want_tables), ("loglik", self.want_ll),
+                                                    ("mi", self.want_mi)) if f)}
+
+    def cpu_baseline(self, budget, threads):
+        limit = 12_500_000 if self.w.m > 20_000_000 else None
+
+        def cols_fn(vs, nrows):  # the very columns the GPU counted (download is untimed)
+            return np.vstack([self.gdb.download(v, 0, nrows) for v in vs])
+
+        return cpu_rate_queries(self.w, self.queries, budget, threads, row_limit=limit, cols_fn=cols_fn)
+
+
+class ItemsetRunner:
+    """cfg4: supports of all 2- and 3-itemsets of the top-200 items (one k_itemsets launch)."""
+
+    kernel = "k_itemsets"
+
+    def __init__(self, args, world, rank, local, torch, ctx):
+        from paper_1804_04640_b200 import workloads as W
+
+        self.torch, self.ctx, self.world, self.rank = torch, ctx, world, rank
+        self.config = "cfg4"
+        m = args.m or 10_000_000
+        self.w = W.cfg4(m=m)
+        w = self.w
+        t0 = time.perf_counter()
+        self.gdb = w.build_device(ctx)
+        sup = self.gdb.count_points([((v,), (1,)) for v in range(w.n)])
+        self.items = W.select_top_items(sup, w.meta["top"])
+        self.gdb.bitmap_build(self.items)
+        ctx.sync()
+        self.build_s = time.perf_counter() - t0
+        k = len(self.items)
+        self.npairs = k * (k - 1) // 2
+        self.ntri = k * (k - 1) * (k - 2) // 6
+        self.units = self.npairs + self.ntri
+        words = (m + 31) // 32
+        self.algo_bytes = float(self.npairs * 2 + self.ntri * 3) * words * 4
+        dev = "cuda"
+        self.pairs = torch.empty((k, k), dtype=torch.int64, device=dev)
+        self.triples = torch.empty(self.ntri, dtype=torch.int64, device=dev)
+        self.h_pairs = torch.empty((k, k), dtype=torch.int64, pin_memory=True)
+        self.h_triples = torch.empty(self.ntri, dtype=torch.int64, pin_memory=True)
+        self.h2d = 4 * k
+        self.d2h = 8 * (k * k + self.ntri)
+        self.scaling = "weak"
+        self.parallelism = "replica" if world == 1 else f"replicas x{world}"
+
+    def step(self):
+        self.gdb.itemset_supports(self.items, self.pairs, self.triples)
+
+    def e2e_step(self):
+        self.gdb.itemset_supports(self.items, self.h_pairs, self.h_triples)
+
+    def describe(self):
+        return {"workload": "cfg4", "items": self.w.n, "m": self.w.m, "top": len(self.items),
+                "itemsets_per_step": self.units, "parallelism": self.parallelism,
+                "outputs": "pair+triple supports", "zipf_c": round(self.w.meta["zipf_c"], 6)}
+
+    def cpu_baseline(self, budget, threads):
+        """bitmap_count restatement on planes of the same items (downloaded columns), sampled."""
+        import itertools
+
+        O = _oracle()
+        rows = min(self.w.m, 2_000_000)
+        cols = {v: self.gdb.download(v, 0, rows) for v in self.items}
+        planes = {(v, 1): O.bitmap_planes(cols[v], 1) for v in self.items}
+        its = list(itertools.combinations(self.items, 3))
+        probe = [tuple((v, 1) for v in t) for t in its[:2000]]
+        t0 = time.perf_counter()
+        O.bitmap_counts(planes, probe, rows, nthreads=threads)
+        rate = len(probe) / (time.perf_counter() - t0)
+        n = int(min(len(its), max(len(probe), rate * budget)))
+        sample = [tuple((v, 1) for v in t) for t in its[:: max(1, len(its) // n)][:n]]
+        t0 = time.perf_counter()
+        O.bitmap_counts(planes, sample, rows, nthreads=threads)
+        dt = time.perf_counter() - t0
+        scale = rows / self.w.m
+        return (len(sample) / dt * scale,
+                f"{len(sample)} 3-itemsets on the first {rows} rows in {dt:.1f} s (bitmap_count restatement "
+                f"oracle_bitmap_counts, {threads} threads; rate scaled x{scale:g} to m={self.w.m})")
+
+
+# ---------------------------------------------------------------------------------------------
+# arms
 
 
 def run_reference(args, world, rank):
     """--impl reference: the CPU port of the reference path, rank 0 only."""
     if rank != 0:
         return
-    w, queries = build_workload(args.config, 1, 0, args.nq)
-    cols = host_columns(w)
     threads = os.cpu_count() or 1
-    rates = []
-    samples = []
+    if args.config == "cfg4":
+        raise SystemExit("--impl reference supports the query configs (default cfg2)")
+    w, queries = workload(args.config, 1, 0, args.nq)
+    limit = 12_500_000 if w.m > 20_000_000 else None
+    rates, descs = [], []
     for i in range(args.warmup + args.steps):
-        rate, n, dt = cpu_sample_rate(cols, w.arities, queries[(i * 97) % max(len(queries) - 1, 1):] + queries,
-                                      args.ref_budget, threads)
+        rot = (i * 997) % max(len(queries), 1)
+        qs = list(queries[rot:]) + list(queries[:rot])
+        rate, desc = cpu_rate_queries(w, qs, args.ref_budget, threads, row_limit=limit)
         if i >= args.warmup:
             rates.append(rate)
-            samples.append(n)
+            descs.append(desc)
     v = statistics.mean(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * len(queries) / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": {"workload": w.name, "m": w.m, "n": w.n, "queries": len(queries)},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{int(statistics.mean(samples))} queries of {w.name} per step "
-                                   "(oracle/radix_oracle.c, C restatement of radix_query, "
-                                   f"{threads} threads)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": descs[-1]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -208,9 +407,7 @@ def run_reference(args, world, rank):
 def run_ours(args, world, rank, local):
     import torch
 
-    import paper_1804_04640_b200 as cs
-    from paper_1804_04640_b200 import _native as N
-    from paper_1804_04640_b200.engine import GpuContext, QueryPlan, encode_queries
+    from paper_1804_04640_b200.engine import GpuContext
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -218,32 +415,15 @@ def run_ours(args, world, rank, local):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = GpuContext(local)
-    # a non-default stream: CUDA events and the library's launches share it
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.Stream()  # non-default: CUDA events and the library share it
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-
-    w, queries = build_workload(args.config, world, rank, args.nq)
-    t0 = time.perf_counter()
-    gdb = w.build_device(ctx)
-    ctx.sync()
-    build_s = time.perf_counter() - t0
-
-    want_tables = args.config in ("cfg1", "cfg2")
-    want_ll = args.config in ("cfg1", "cfg3")
-    flags = N.CS_WANT_TABLES if want_tables else 0
-    plan = QueryPlan(gdb, queries, flags)
-    nq = plan.nq
-    tables = torch.empty(max(plan.total_cells, 1), dtype=torch.int32, device="cuda") if want_tables else None
-    ll = torch.empty(nq, dtype=torch.float64, device="cuda") if want_ll else None
+    R = ItemsetRunner if args.config == "cfg4" else QueryRunner
+    r = R(args, world, rank, local, torch, ctx)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    algo_bytes = float(sum(len(q) for q in queries)) * w.m
-
-    def step():
-        plan.execute(tables=tables, loglik=ll)
 
     for _ in range(args.warmup):
-        step()
+        r.step()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -256,35 +436,26 @@ def run_ours(args, world, rank, local):
         for i in range(args.steps):
             flush.fill_(i)  # evict the database from L2 before every timed step (untimed)
             starts[i].record(stream)
-            step()
+            r.step()
             ends[i].record(stream)
-            kernel_ms.append(ctx.last_kernel_ms())  # k_hist alone (library events, same stream)
+            kernel_ms.append(ctx.last_kernel_ms())  # dominant kernel alone (library events)
         torch.cuda.synchronize()
     launches = ctx.launches - l0
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    # diagnostic: back-to-back steps without the L2 flush (not the reported value)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(3):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    warm_ms = e0.elapsed_time(e1) / 3
     step_ms = float(np.mean(ms))
+    k_ms = float(np.mean(kernel_ms)) if kernel_ms and min(kernel_ms) > 0 else step_ms
     if world > 1:
-        t = torch.tensor([step_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([step_ms, k_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        step_ms = float(t.item())
+        step_ms, k_ms = (float(x) for x in t.tolist())
 
-    # e2e through the C ABI with host buffers (pinned), per step
-    off, flat = encode_queries(queries)
-    h_tables = torch.empty(max(plan.total_cells, 1), dtype=torch.int32, pin_memory=True) if want_tables else None
-    h_ll = torch.empty(nq, dtype=torch.float64, pin_memory=True) if want_ll else None
     e2e_ms = []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        gdb.query_batch(off, flat, flags, tables=h_tables, loglik=h_ll)
+        r.e2e_step()
         dt = (time.perf_counter() - t0) * 1e3
         if i >= args.warmup:
             e2e_ms.append(dt)
@@ -293,42 +464,35 @@ def run_ours(args, world, rank, local):
         t = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_step = float(t.item())
-    h2d = int(off.nbytes + flat.nbytes)
-    d2h = int((plan.total_cells * 4 if want_tables else 0) + (nq * 8 if want_ll else 0))
 
-    total_q = nq * world
-    value = total_q / (step_ms / 1e3)
-    e2e_value = total_q / (e2e_step / 1e3)
+    sharded = getattr(r, "sharded", False)
+    total = r.units if sharded else r.units * world
+    value = total / (step_ms / 1e3)
     peak, peak_src = load_peaks()
-    k_ms = float(np.mean(kernel_ms)) if kernel_ms and min(kernel_ms) > 0 else step_ms
-    achieved = algo_bytes / (k_ms / 1e3) / 1e9
+    achieved = r.algo_bytes / (k_ms / 1e3) / 1e9
+    cfg = r.describe()
+    cfg.update({"l2": "flushed (256 MB write) before every timed step", "db_build_seconds": round(r.build_s, 3)})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "queries_per_gpu": nq,
-                   "total_cells_per_gpu": int(plan.total_cells), "parallelism": f"query-shard x{world}",
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "outputs": ("tables" if want_tables else "") + ("+loglik" if want_ll else ""),
-                   "db_build_seconds": round(build_s, 3)},
-        "scanned_gbs": achieved * world,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "kernel_ms": k_ms,
-                     "frac": achieved / peak, "traffic": load_traffic(w.name),
-                     "kernel": "k_hist", "peak_source": peak_src,
-                     "note": "algorithmic bytes = sum_q k_q*m per launch; >1 means L2 reuse across queries"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "cs_query_batch, host descriptors in, pinned host tables out"},
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": r.scaling,
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded; DESIGN.md Workloads)",
+        "config": cfg,
+        "scanned_gbs": r.algo_bytes * world / (step_ms / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": load_traffic(r.config), "kernel": r.kernel,
+                     "kernel_ms": k_ms, "peak_source": peak_src,
+                     "note": "achieved = algorithmic bytes per launch / kernel time; frac > 1 means the "
+                             "kernel reuses data from L2/SMEM across queries (reuse regime)"},
+        "e2e": {"value": total / (e2e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": r.h2d,
+                "d2h_bytes_per_step": r.d2h, "ms_per_step": e2e_step},
         "gpu_launches": launches,
-        "diag": {"step_ms": [round(x, 4) for x in ms[:10]], "warm_l2_step_ms": round(warm_ms, 4)},
+        "diag": {"step_ms": [round(x, 4) for x in ms[:8]]},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cols = host_columns(w)
         threads = os.cpu_count() or 1
-        rate, n, dt = cpu_sample_rate(cols, w.arities, queries, args.ref_budget, threads)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"first {n} of {nq} {w.name} queries ({dt:.1f} s; "
-                                          "oracle/radix_oracle.c radix restatement)"}
+        rate, desc = r.cpu_baseline(args.ref_budget, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -340,18 +504,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nq", type=int, default=None, help="queries per GPU (default: the config's)")
-    ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of CPU work per sample")
+    ap.add_argument("--nq", type=int, default=None, help="queries per GPU per step (default: the config's)")
+    ap.add_argument("--m", type=int, default=None, help="rows (cfg4 only; default 1e7)")
+    ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_env()
     if args.impl == "reference":
-        args.ref_budget = min(args.ref_budget, 8.0)
+        args.ref_budget = min(args.ref_budget, 6.0)
         run_reference(args, world, rank)
         return
+    args.warmup = max(args.warmup, 3)
     run_ours(args, world, rank, local)
 
 

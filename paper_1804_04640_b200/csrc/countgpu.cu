@@ -16,6 +16,7 @@
 #include "../../include/countstream_gpu.h"
 #include "cs_common.cuh"
 #include "cs_kernels.cuh"
+#include "cs_itemsets.cuh"
 
 using namespace cs;
 
@@ -1039,6 +1040,76 @@ extern "C" int cs_count_points(cs_db* db, int32_t nq, const int32_t* var_off, co
 
 extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* items, int64_t* pairs,
                                    int64_t* triples) {
-  (void)db; (void)nitems; (void)items; (void)pairs; (void)triples;
-  return fail(CS_ERR_UNSUPPORTED, "cs_itemset_supports: not built yet");
+  if (!db) return fail(CS_ERR_INVALID, "cs_itemset_supports: NULL db");
+  if (nitems < 0 || nitems > 30000) return fail(CS_ERR_INVALID, "cs_itemset_supports: nitems %d", nitems);
+  if (nitems == 0 || (!pairs && !triples)) return CS_OK;
+  if (!items) return fail(CS_ERR_INVALID, "cs_itemset_supports: items is NULL");
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  const int n = nitems;
+  std::vector<const uint32_t*> hp(n);
+  for (int i = 0; i < n; ++i) {
+    const int v = items[i];
+    if (v < 0 || v >= db->n) return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
+    if (db->arity[v] < 2) return fail(CS_ERR_INVALID, "item %d has no state 1 (arity %d)", v, db->arity[v]);
+    if (db->plane_off[v] < 0)
+      return fail(CS_ERR_INVALID, "item %d has no bit planes; call cs_bitmap_build first", v);
+    hp[i] = db->planes + db->plane_off[v] + db->words;  // state-1 plane
+  }
+  // rows: singles (a, a) -> pair supports, pairs (a, b) -> triple supports; sorted by b
+  std::vector<ISRow> rows;
+  rows.reserve((size_t)n * (n + 1) / 2);
+  for (int b = 0; b < n; ++b) {
+    rows.push_back(ISRow{(int16_t)b, (int16_t)b});
+    for (int a = 0; a < b; ++a) rows.push_back(ISRow{(int16_t)a, (int16_t)b});
+  }
+  const int nrows = (int)rows.size();
+  std::vector<std::pair<int, int>> tiles;
+  for (int r0 = 0; r0 < nrows; r0 += IS_ROWS) {
+    const int minb = rows[r0].b;
+    for (int c0 = ((minb + 1) / IS_COLS) * IS_COLS; c0 < n; c0 += IS_COLS) tiles.emplace_back(r0, c0);
+  }
+  const int64_t W = db->words;  // multiple of 32 words
+  const int64_t target = 4LL * 2 * ctx->num_sms;
+  int64_t S = std::max<int64_t>(1, (target + (int64_t)tiles.size() - 1) / std::max<int64_t>(1, tiles.size()));
+  S = std::min<int64_t>(S, W / IS_TW);
+  const int64_t slice = ((W / S + IS_TW - 1) / IS_TW) * IS_TW;
+  std::vector<ISUnit> units;
+  for (int64_t w0 = 0; w0 < W; w0 += slice)
+    for (auto& t : tiles) units.push_back(ISUnit{t.first, t.second, w0, std::min(W, w0 + slice)});
+  const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
+  const size_t bp = sizeof(void*) * n, br = sizeof(ISRow) * nrows, bu = sizeof(ISUnit) * units.size();
+  const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
+  size_t off = 0;
+  auto place = [&](size_t b) {
+    size_t o = off;
+    off = round_up(off + b, 256);
+    return o;
+  };
+  const size_t op = place(bp), orr = place(br), ou = place(bu), oh = place(256), opr = place(bpairs),
+               otr = place(btri);
+  void* blob = nullptr;
+  CS_TRY(ctx->scratch_get(10, off, &blob));
+  char* d = (char*)blob;
+  CS_CUDA(cudaMemcpyAsync(d + op, hp.data(), bp, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemcpyAsync(d + orr, rows.data(), br, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemcpyAsync(d + ou, units.data(), bu, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d + oh, 0, 256, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d + opr, 0, bpairs + (otr - opr - bpairs) + btri, ctx->stream));
+  const int grid = (int)std::min<int64_t>((int64_t)units.size(), 2LL * ctx->num_sms);
+  CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+  k_itemsets<<<grid, IS_THREADS, 0, ctx->stream>>>((const uint32_t* const*)(d + op), (const ISRow*)(d + orr),
+                                                   nrows, n, (const ISUnit*)(d + ou), (int)units.size(),
+                                                   (int*)(d + oh), (unsigned long long*)(d + opr),
+                                                   (unsigned long long*)(d + otr));
+  CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->ev_valid = true;
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  const cudaMemcpyKind kp = is_device_ptr(pairs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const cudaMemcpyKind kt = is_device_ptr(triples) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (pairs) CS_CUDA(cudaMemcpyAsync(pairs, d + opr, bpairs, kp, ctx->stream));
+  if (triples && ntri) CS_CUDA(cudaMemcpyAsync(triples, d + otr, sizeof(uint64_t) * ntri, kt, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
 }

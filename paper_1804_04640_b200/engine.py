@@ -188,11 +188,16 @@ class GpuDatabase:
         return out
 
     def itemset_supports(self, items: Sequence[int], pairs: bool = True, triples: bool = True):
+        """Supports of every 2- and 3-subset of ``items`` in state 1 (planes must exist).
+
+        Returns (pairs (k, k) int64 with [a, b] filled for a < b, triples int64 in
+        itertools.combinations order).  Outputs may also be given as device tensors.
+        """
         it = np.ascontiguousarray(list(items), dtype=np.int32)
         k = len(it)
-        pr = np.zeros((k, k), dtype=np.int64) if pairs else None
+        pr = (np.zeros((k, k), dtype=np.int64) if pairs is True else pairs) if pairs is not False else None
         ntri = k * (k - 1) * (k - 2) // 6
-        tr = np.zeros(ntri, dtype=np.int64) if triples else None
+        tr = (np.zeros(ntri, dtype=np.int64) if triples is True else triples) if triples is not False else None
         check(lib.cs_itemset_supports(self._h, k, ptr(it), ptr(pr), ptr(tr)))
         return pr, tr
 

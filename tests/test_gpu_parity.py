@@ -236,3 +236,45 @@ def test_properties_full_size(ctx):
         s = tabs[plan.table_off[j]:plan.table_off[j] + plan.cells[j]].astype(np.int64)
         last = int(w.arities[qs[i][-1]])
         assert np.array_equal(t.reshape(last, -1).sum(axis=0), s)
+
+
+def test_itemset_supports_all_pairs_triples(ctx):
+    """cs_itemset_supports (Harley-Seal bit-GEMM) vs the bitmap_count restatement."""
+    import itertools
+
+    rng = np.random.default_rng(17)
+    n_items, m = 45, 100_003
+    p = np.clip(0.6 * np.arange(1, n_items + 1) ** -0.7, 0.01, 1.0)
+    u8 = (rng.random((n_items, m)) < p[:, None]).astype(np.uint8)
+    gdb = GpuDatabase.from_columns(ctx, u8, [2] * n_items)
+    gdb.bitmap_build()
+    items = list(range(3, n_items))  # a subset, not starting at 0
+    pr, tr = gdb.itemset_supports(items)
+    planes = {(v, 1): O.bitmap_planes(u8[v], 1) for v in items}
+    pairs = list(itertools.combinations(range(len(items)), 2))
+    want_p = O.bitmap_counts(planes, [((items[a], 1), (items[b], 1)) for a, b in pairs], m)
+    assert [int(pr[a, b]) for a, b in pairs] == want_p.tolist()
+    triples = list(itertools.combinations(range(len(items)), 3))
+    want_t = O.bitmap_counts(planes, [tuple((items[x], 1) for x in t) for t in triples], m)
+    assert np.array_equal(tr, want_t)
+    # point-count path agrees on a sample
+    sample = triples[::97]
+    got = gdb.count_points([([items[x] for x in t], [1, 1, 1]) for t in sample])
+    assert got.tolist() == [int(want_t[triples.index(t)]) for t in sample]
+
+
+def test_cfg4_workload_small(ctx):
+    """configs[3] generator + top-k selection + supports at reduced m."""
+    w = workloads.cfg4(m=200_000, n_items=300, top=40)
+    gdb = w.build_device(ctx)
+    sup = gdb.count_points([((v,), (1,)) for v in range(w.n)])
+    rows = np.arange(w.m)
+    cols = gen_twin.generate_workload_columns(w, rows)
+    assert sup.tolist() == [int(cols[v].sum()) for v in range(w.n)]
+    top = workloads.select_top_items(sup, 40)
+    gdb.bitmap_build(top)
+    pr, tr = gdb.itemset_supports(top)
+    planes = {(v, 1): O.bitmap_planes(cols[v], 1) for v in top}
+    its = workloads.itemsets_of(range(len(top)), (3,))
+    want = O.bitmap_counts(planes, [tuple((top[x], 1) for x in t) for t in its], w.m)
+    assert np.array_equal(tr, want)
