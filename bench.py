@@ -231,8 +231,9 @@ class QueryRunner:
         self.sharded = args.config == "cfg5" and world > 1
         t0 = time.perf_counter()
         if self.sharded:
-            per = (w.m + world - 1) // world
-            self.row0, self.rows = rank * per, min(per, w.m - rank * per)
+            from paper_1804_04640_b200.parallel import shard_rows
+
+            self.row0, self.rows = shard_rows(w.m, world, rank)
             self.gdb = w.build_device(ctx, row_offset=self.row0, m_shard=self.rows)
         else:
             self.rows = w.m
@@ -269,8 +270,10 @@ class QueryRunner:
 
     def step(self):
         if self.sharded:
+            from paper_1804_04640_b200.parallel import merge_tables_
+
             self.plan.execute(tables=self.tables)
-            self.torch.distributed.all_reduce(self.tables)  # uint32 sum == int32 sum bitwise
+            merge_tables_(self.tables)  # NCCL all-reduce; uint32 sum == int32 sum bitwise
             self.plan.score(self.tables, loglik=self.ll, mi=self.mi)
         else:
             self.plan.execute(tables=self.tables, loglik=self.ll, mi=self.mi)
@@ -298,6 +301,74 @@ class QueryRunner:
             return np.vstack([self.gdb.download(v, 0, nrows) for v in vs])
 
         return cpu_rate_queries(self.w, self.queries, budget, threads, row_limit=limit, cols_fn=cols_fn)
+
+
+class FamilyRunner:
+    """cfg3: MDL + LL of every (X_i, Pa), |Pa| <= 3 (288,859 families) via the N ln N sums of
+    the 74,518 distinct variable subsets (one k_hist launch + k_family)."""
+
+    kernel = "k_hist"
+
+    def __init__(self, args, world, rank, local, torch, ctx):
+        from paper_1804_04640_b200 import _native as N
+        from paper_1804_04640_b200 import workloads as W
+        from paper_1804_04640_b200.engine import FamilyScorer, encode_queries
+
+        self.torch, self.ctx, self.world, self.rank = torch, ctx, world, rank
+        self.config = "cfg3"
+        self.N = N
+        self.w = W.cfg3()
+        w = self.w
+        fams = [(q[0], tuple(q[1:])) for q in w.queries][rank::world]
+        if args.nq:
+            fams = fams[: args.nq]
+        t0 = time.perf_counter()
+        self.gdb = w.build_device(ctx)
+        ctx.sync()
+        self.build_s = time.perf_counter() - t0
+        self.fs = FamilyScorer(self.gdb, fams)
+        self.h_sidx, self.h_pidx, self.h_pen = self.fs.s_idx, self.fs.p_idx, self.fs.penalty
+        self.fs.to_device(torch)
+        self.units = self.fs.nfam
+        self.nlogn = torch.empty(self.fs.nsub, dtype=torch.float64, device="cuda")
+        self.ll = torch.empty(self.units, dtype=torch.float64, device="cuda")
+        self.mdl = torch.empty(self.units, dtype=torch.float64, device="cuda")
+        self.algo_bytes = float(sum(len(s) for s in self.fs.subsets)) * w.m
+        self.family_bytes = float(sum(1 + len(p) for _, p in fams)) * w.m
+        self.off, self.flat = encode_queries(self.fs.subsets)
+        pin = dict(pin_memory=True)
+        self.h_nlogn = torch.empty(self.fs.nsub, dtype=torch.float64, **pin)
+        self.h_ll = torch.empty(self.units, dtype=torch.float64, **pin)
+        self.h_mdl = torch.empty(self.units, dtype=torch.float64, **pin)
+        self.h2d = int(self.off.nbytes + self.flat.nbytes + self.h_sidx.nbytes + self.h_pidx.nbytes
+                       + self.h_pen.nbytes)
+        self.d2h = int(self.units * 16 + self.fs.nsub * 8)
+        self.scaling = "weak"
+        self.parallelism = f"family-shard x{world}"
+
+    def step(self):
+        self.fs.run(self.nlogn, self.ll, self.mdl)
+
+    def e2e_step(self):
+        from paper_1804_04640_b200._native import check, lib, ptr
+
+        self.gdb.query_batch(self.off, self.flat, self.N.CS_NLOGN, loglik=self.h_nlogn)
+        check(lib.cs_family_scores(self.ctx.handle, self.units, ptr(self.h_nlogn), self.fs.nsub,
+                                   ptr(self.h_sidx), ptr(self.h_pidx), ptr(self.h_pen), self.fs.m_ln_m,
+                                   ptr(self.h_ll), ptr(self.h_mdl)))
+
+    def describe(self):
+        return {"workload": "cfg3", "n": self.w.n, "m": self.w.m, "families_per_step": self.units,
+                "distinct_subsets": self.fs.nsub, "parallelism": self.parallelism, "outputs": "loglik+mdl",
+                "family_logical_bytes": self.family_bytes,
+                "method": "LL(X|Pa) = sum n ln n over joint(X u Pa) - over joint(Pa)"}
+
+    def cpu_baseline(self, budget, threads):
+        def cols_fn(vs, nrows):
+            return np.vstack([self.gdb.download(v, 0, nrows) for v in vs])
+
+        qs = [(t, *ps) for t, ps in self.fs.families]
+        return cpu_rate_queries(self.w, qs, budget, threads, cols_fn=cols_fn)
 
 
 class ItemsetRunner:
@@ -418,7 +489,7 @@ def run_ours(args, world, rank, local):
     stream = torch.cuda.Stream()  # non-default: CUDA events and the library share it
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    R = ItemsetRunner if args.config == "cfg4" else QueryRunner
+    R = {"cfg4": ItemsetRunner, "cfg3": FamilyRunner}.get(args.config, QueryRunner)
     r = R(args, world, rank, local, torch, ctx)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
 

@@ -54,6 +54,9 @@ extern "C" {
 #define CS_WANT_MI 0x4u      /* fp64 mutual information I(X_t; Pa) in nats (new, survey 8a) */
 #define CS_WANT_NNZ 0x8u     /* number of non-zero cells (NullSink.count, aggregators.py:80-93) */
 #define CS_PARTIAL 0x10u     /* shard-local tables only: skip scores (merge then cs_plan_score) */
+#define CS_NLOGN 0x20u       /* loglik output = sum over cells of N ln N (joint-table "entropy
+                              * numerator"); LL(X|Pa) = NLOGN(X u Pa) - NLOGN(Pa), which lets a
+                              * batch score every family from the distinct variable subsets */
 
 typedef struct cs_ctx cs_ctx;   /* one device + one stream + scratch */
 typedef struct cs_db cs_db;     /* device-resident database (one instance shard) */
@@ -70,8 +73,8 @@ int cs_ctx_set_stream(cs_ctx* ctx, void* stream);
 int cs_ctx_sync(cs_ctx* ctx);
 /* number of kernels this context has launched so far (bench `gpu_launches`) */
 int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches);
-/* device time (ms, CUDA events on the context stream) of the last K1 histogram launch;
- * waits for it to finish.  0 if none yet. */
+/* device time (ms, CUDA events on the context stream) of the last histogram phase (all K1
+ * launches of one cs_plan_execute) or itemset launch; waits for it.  0 if none yet. */
 int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms);
 /* number of SMs / bytes of dynamic smem the histogram kernel uses (diagnostics) */
 int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_bytes, int32_t* hist_ctas);
@@ -132,6 +135,13 @@ int cs_plan_destroy(cs_plan* plan);
 /* create + execute + destroy */
 int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                    uint32_t flags, uint32_t* tables, double* loglik, double* mi, int64_t* nnz);
+
+/* Batched MDL parent-set scoring (learn_parents, harness.py:296-348; MdlScore,
+ * aggregators.py:163-193).  nlogn[nsub]: CS_NLOGN outputs of a plan over the distinct variable
+ * subsets; family f scores  ll[f] = nlogn[s_idx[f]] - (p_idx[f] >= 0 ? nlogn[p_idx[f]] : m_ln_m)
+ * and mdl[f] = -ll[f] + penalty[f].  Inputs/outputs host or device. */
+int cs_family_scores(cs_ctx* ctx, int64_t nfam, const double* nlogn, int64_t nsub, const int32_t* s_idx,
+                     const int32_t* p_idx, const double* penalty, double m_ln_m, double* ll, double* mdl);
 
 /* ---- point counts / itemset supports (reference bitmap.py:131-136, radix.py:181-193) - */
 /* counts[q] = #records with vars[j] == states[j] for every j in query q.  Uses bitmap

@@ -26,6 +26,7 @@ CS_WANT_LOGLIK = 0x2
 CS_WANT_MI = 0x4
 CS_WANT_NNZ = 0x8
 CS_PARTIAL = 0x10
+CS_NLOGN = 0x20
 
 # (name, restype, argtypes) for every symbol declared in include/countstream_gpu.h
 _P = c_void_p
@@ -56,6 +57,7 @@ SIGNATURES = [
     ("cs_plan_score", c_int, [_P, _P, _P, _P, _P]),
     ("cs_plan_compact", c_int, [_P, _P, _P, c_int64, _P, _P, _P]),
     ("cs_plan_destroy", c_int, [_P]),
+    ("cs_family_scores", c_int, [_P, c_int64, _P, c_int64, _P, _P, _P, c_double, _P, _P]),
     ("cs_query_batch", c_int, [_P, c_int32, _P, _P, c_uint32, _P, _P, _P, _P]),
     ("cs_count_points", c_int, [_P, c_int32, _P, _P, _P, _P]),
     ("cs_itemset_supports", c_int, [_P, c_int32, _P, _P, _P]),

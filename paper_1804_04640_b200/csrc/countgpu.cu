@@ -850,6 +850,8 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   CS_CUDA(cudaMemsetAsync(p->d_head, 0, 256, ctx->stream));
   CS_CUDA(cudaMemsetAsync(p->d_done, 0, sizeof(uint32_t) * p->nq, ctx->stream));
   const double m_total = (double)db->m_total;
+  // ev0/ev1 bracket the whole histogram phase (K1 global + K1 SMEM + K1g) on this stream
+  CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
   if (p->ngitems > 0) {
     const int grid = std::min(2 * ctx->num_sms, p->ngitems);
     k_hist_global<<<grid, 512, 0, ctx->stream>>>(p->d_q, p->d_items + p->nitems, p->ngitems,
@@ -859,7 +861,6 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   }
   if (p->nitems > 0) {
     const int grid = std::min(ctx->hist_ctas, p->nitems);
-    CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
 #define CS_LAUNCH_HIST(T, B, PF)                                                              \
   k_hist<T, B, PF><<<grid, T, ctx->hist_smem, ctx->stream>>>(                                 \
       p->d_q, p->d_items, p->nitems, p->d_head, dtab, p->d_done, (double*)lb.dev, (double*)mb.dev, \
@@ -871,8 +872,6 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
       default: CS_LAUNCH_HIST(384, 2, false); break;
     }
 #undef CS_LAUNCH_HIST
-    CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    ctx->ev_valid = true;
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
   }
@@ -883,6 +882,8 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
   }
+  CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->ev_valid = true;
   if (!partial && !p->score_list.empty() && (flags & (F_LOGLIK | F_MI | F_NNZ))) {
     k_score<<<(unsigned)p->score_list.size(), 256, 0, ctx->stream>>>(
         p->d_q, p->d_score_list, dtab, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev, flags, m_total);
@@ -899,11 +900,11 @@ extern "C" int cs_plan_score(cs_plan* p, const uint32_t* tables, double* loglik,
   cs_ctx* ctx = p->db->ctx;
   CS_CUDA(cudaSetDevice(ctx->device));
   if (p->nq == 0) return CS_OK;
-  uint32_t flags = 0;
+  uint32_t flags = p->flags & F_NLOGN;
   if (loglik) flags |= F_LOGLIK;
   if (mi) flags |= F_MI;
   if (nnz) flags |= F_NNZ;
-  if (!flags) return CS_OK;
+  if (!(flags & (F_LOGLIK | F_MI | F_NNZ))) return CS_OK;
   const uint32_t* dtab = nullptr;
   CS_TRY(input_tables(p, tables, &dtab));
   OutBuf lb, mb, nb;
@@ -943,6 +944,43 @@ extern "C" int cs_plan_compact(cs_plan* p, const uint32_t* tables, const int64_t
   CS_TRY(finish_outputs(ctx, obs, 3));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));  // out_off staging reused next call
   return CS_OK;
+}
+
+// batched learn_parents: family LL / MDL from the N ln N sums of the distinct variable subsets
+extern "C" int cs_family_scores(cs_ctx* ctx, int64_t nfam, const double* nlogn, int64_t nsub,
+                                const int32_t* s_idx, const int32_t* p_idx, const double* penalty,
+                                double m_ln_m, double* ll, double* mdl) {
+  if (!ctx || nfam < 0 || nsub < 0) return fail(CS_ERR_INVALID, "cs_family_scores: bad argument");
+  if (nfam == 0) return CS_OK;
+  if (!nlogn || !s_idx || !p_idx || (mdl && !penalty))
+    return fail(CS_ERR_INVALID, "cs_family_scores: NULL input");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  auto dev_in = [&](const void* src, size_t bytes, int slot, const void** out) -> int {
+    if (is_device_ptr(src)) {
+      *out = src;
+      return CS_OK;
+    }
+    void* d = nullptr;
+    CS_TRY(ctx->scratch_get(slot, bytes, &d));
+    CS_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *out = d;
+    return CS_OK;
+  };
+  const void *dn = nullptr, *ds = nullptr, *dp = nullptr, *dpen = nullptr;
+  CS_TRY(dev_in(nlogn, sizeof(double) * std::max<int64_t>(nsub, 1), 11, &dn));
+  CS_TRY(dev_in(s_idx, sizeof(int32_t) * nfam, 12, &ds));
+  CS_TRY(dev_in(p_idx, sizeof(int32_t) * nfam, 13, &dp));
+  if (mdl) CS_TRY(dev_in(penalty, sizeof(double) * nfam, 14, &dpen));
+  OutBuf lb, mb;
+  CS_TRY(route(ctx, 15, ll, sizeof(double) * nfam, lb));
+  CS_TRY(route(ctx, 16, mdl, sizeof(double) * nfam, mb));
+  const unsigned grid = (unsigned)std::min<int64_t>((nfam + 255) / 256, 65535);
+  k_family<<<grid, 256, 0, ctx->stream>>>(nfam, (const double*)dn, (const int32_t*)ds, (const int32_t*)dp,
+                                          (const double*)dpen, m_ln_m, (double*)lb.dev, (double*)mb.dev);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  OutBuf obs[2] = {lb, mb};
+  return finish_outputs(ctx, obs, 2);
 }
 
 extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,

@@ -48,6 +48,7 @@ enum : uint32_t {
   F_MI = 0x4u,
   F_NNZ = 0x8u,
   F_PARTIAL = 0x10u,
+  F_NLOGN = 0x20u,  // the loglik output receives sum_cells n ln n (joint "entropy numerator")
 };
 
 // Counter-based generator (twin: oracle/gen_twin.py).  splitmix64 finaliser.

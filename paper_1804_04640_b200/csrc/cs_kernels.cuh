@@ -107,7 +107,7 @@ __device__ void score_table(CellFn cell, uint32_t C, int rt, double m_total, uin
       const uint32_t n = cell(base + k);
       if (n) {
         const double x = (double)n;
-        ll += x * log(x / dnij);
+        ll += (flags & F_NLOGN) ? x * log(x) : x * log(x / dnij);
         ++nz;
         if (want_mi) mi += x * log((x * m_total) / (dnij * (double)ss.marg[k]));
       }
@@ -441,6 +441,21 @@ __global__ void k_score(const QDesc* __restrict__ qd, const int32_t* __restrict_
   const uint32_t* t = tables + d.table_off;
   auto cell = [&](uint32_t c) -> uint32_t { return t[c]; };
   score_table(cell, d.cells, d.r_target, m_total, flags, q, ll_out, mi_out, nnz_out, ss);
+}
+
+// family scores for the batched learn_parents driver (harness.py:296-348 semantics):
+//   LL(X | Pa) = sum n ln n over joint(X u Pa) - sum n ln n over joint(Pa)
+// (the second term is m ln m for Pa = {}), MDL = -LL + penalty (aggregators.py:191-193).
+__global__ void k_family(int64_t nfam, const double* __restrict__ nlogn,
+                         const int32_t* __restrict__ s_idx, const int32_t* __restrict__ p_idx,
+                         const double* __restrict__ penalty, double m_ln_m, double* ll, double* mdl) {
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nfam;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t pi = p_idx[f];
+    const double v = nlogn[s_idx[f]] - (pi >= 0 ? nlogn[pi] : m_ln_m);
+    if (ll) ll[f] = v;
+    if (mdl) mdl[f] = -v + penalty[f];
+  }
 }
 
 // K5: non-zero cells of each table in ascending cell order.  One CTA per query.

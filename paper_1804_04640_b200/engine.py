@@ -8,6 +8,7 @@ or torch CUDA tensors (device); outputs land wherever the caller's array lives.
 from __future__ import annotations
 
 import ctypes
+import math
 from ctypes import byref, c_int32, c_int64, c_void_p
 from typing import Iterable, Sequence
 
@@ -16,7 +17,7 @@ import numpy as np
 from . import _native as N
 from ._native import check, lib, ptr
 
-__all__ = ["GpuContext", "GpuDatabase", "QueryPlan", "encode_queries"]
+__all__ = ["GpuContext", "GpuDatabase", "QueryPlan", "FamilyScorer", "encode_queries"]
 
 
 def encode_queries(queries: Iterable[Sequence[int]]) -> tuple[np.ndarray, np.ndarray]:
@@ -270,3 +271,64 @@ class QueryPlan:
             self.close()
         except Exception:
             pass
+
+
+class FamilyScorer:
+    """LL and MDL of many (target, parents) families from one histogram launch.
+
+    LL(X | Pa) = sum_cells n ln n over joint(X u Pa) - sum_cells n ln n over joint(Pa), so a
+    batch of families needs only its *distinct variable subsets* counted (for every parent set
+    of size <= 3 over n=37 variables: 74,518 subsets for 288,859 families).  The subset sums
+    come from a CS_NLOGN plan; cs_family_scores combines them and adds the MDL penalty
+    0.5 ln(m) (r_i - 1) q_i (aggregators.py:191-193).
+    """
+
+    def __init__(self, db: GpuDatabase, families, m_total: int | None = None):
+        self.db = db
+        fams = [(int(t), tuple(int(p) for p in ps)) for t, ps in families]
+        index: dict = {}
+        s_idx = np.empty(len(fams), dtype=np.int32)
+        p_idx = np.empty(len(fams), dtype=np.int32)
+        pen = np.empty(len(fams), dtype=np.float64)
+        m = int(m_total if m_total is not None else db.m_total)
+        lnm = math.log(m)
+        ar = db.arities
+        for f, (t, ps) in enumerate(fams):
+            key = tuple(sorted((t,) + ps))
+            s_idx[f] = index.setdefault(key, len(index))
+            if ps:
+                pk = tuple(sorted(ps))
+                p_idx[f] = index.setdefault(pk, len(index))
+            else:
+                p_idx[f] = -1
+            q_i = 1
+            for p in ps:
+                q_i *= int(ar[p])
+            pen[f] = 0.5 * lnm * (int(ar[t]) - 1) * q_i
+        self.families = fams
+        self.subsets = list(index)
+        self.s_idx, self.p_idx, self.penalty = s_idx, p_idx, pen
+        self.m_ln_m = m * lnm
+        self.plan = QueryPlan(db, self.subsets, N.CS_NLOGN)
+        self.nfam = len(fams)
+        self.nsub = len(self.subsets)
+
+    def to_device(self, torch):
+        """Move the per-family index/penalty arrays to the device (bench: resident inputs)."""
+        self.s_idx = torch.from_numpy(self.s_idx).cuda()
+        self.p_idx = torch.from_numpy(self.p_idx).cuda()
+        self.penalty = torch.from_numpy(self.penalty).cuda()
+        return self
+
+    def run(self, nlogn, ll=None, mdl=None) -> None:
+        """nlogn: float64[nsub] work array (host or device); ll / mdl: float64[nfam] outputs."""
+        self.plan.execute(loglik=nlogn)
+        check(lib.cs_family_scores(self.db.ctx.handle, self.nfam, ptr(nlogn), self.nsub, ptr(self.s_idx),
+                                   ptr(self.p_idx), ptr(self.penalty), self.m_ln_m, ptr(ll), ptr(mdl)))
+
+    def scores(self) -> tuple[np.ndarray, np.ndarray]:
+        nl = np.zeros(self.nsub)
+        ll = np.zeros(self.nfam)
+        mdl = np.zeros(self.nfam)
+        self.run(nl, ll, mdl)
+        return ll, mdl

@@ -26,7 +26,7 @@ import numpy as np
 
 from .aggregators import LogLikelihood, MdlScore, MutualInformation, NullSink
 from .database import Assignment, Database, InvalidQueryError, QuerySpec
-from .engine import GpuContext, GpuDatabase, QueryPlan
+from .engine import FamilyScorer, GpuContext, GpuDatabase, QueryPlan
 from . import _native as N
 
 __all__ = [
@@ -102,6 +102,11 @@ _FUSED_NAMES = {"LogLikelihood": "loglik", "MdlScore": "mdl", "NullSink": "nnz",
 _FUSED_MODULES = {LogLikelihood.__module__, "countstream.aggregators"}
 
 
+def _vars(q) -> tuple:
+    """Index-digit order of a query object (ours or the reference's QuerySpec): target first."""
+    return (int(q.target), *(int(p) for p in q.parents))
+
+
 def _fusion_kind(agg) -> str | None:
     t = type(agg)
     if t.__module__ in _FUSED_MODULES and t.__name__ in _FUSED_NAMES:
@@ -155,7 +160,7 @@ class GpuStrategy(Strategy):
         kind = _fusion_kind(agg)
         with self._lock:
             if kind is not None:
-                plan = QueryPlan(self.gdb, [q.variables])
+                plan = QueryPlan(self.gdb, [_vars(q)])
                 ll = np.zeros(1)
                 mi = np.zeros(1)
                 nnz = np.zeros(1, dtype=np.int64)
@@ -163,7 +168,7 @@ class GpuStrategy(Strategy):
                 plan.close()
                 _absorb(agg, kind, float(ll[0]), float(mi[0]), int(nnz[0]))
                 return
-            plan = QueryPlan(self.gdb, [q.variables], N.CS_WANT_TABLES)
+            plan = QueryPlan(self.gdb, [_vars(q)], N.CS_WANT_TABLES)
             nnz = np.zeros(1, dtype=np.int64)
             plan.execute(nnz=nnz)
             _, cidx, nijk, nij = plan.compact(None, nnz)
@@ -202,7 +207,7 @@ class GpuStrategy(Strategy):
         for q in qs:
             q.validate(self.db)
         with self._lock:
-            plan = QueryPlan(self.gdb, [q.variables for q in qs], N.CS_WANT_TABLES if tables else 0)
+            plan = QueryPlan(self.gdb, [_vars(q) for q in qs], N.CS_WANT_TABLES if tables else 0)
             out = {}
             ll = np.zeros(len(qs)) if loglik else None
             mv = np.zeros(len(qs)) if mi else None
@@ -213,6 +218,18 @@ class GpuStrategy(Strategy):
             out.update({"loglik": ll, "mi": mv, "nnz": nz, "tables": tb,
                         "cells": plan.cells, "table_off": plan.table_off})
             plan.close()
+        return out
+
+    def family_scores(self, families) -> tuple[np.ndarray, np.ndarray]:
+        """(LL, MDL) of many (target, parents) families from one launch over their distinct
+        variable subsets (see engine.FamilyScorer)."""
+        fams = [(int(t), tuple(ps)) for t, ps in families]
+        for t, ps in fams:
+            QuerySpec(t, ps).validate(self.db)
+        with self._lock:
+            fs = FamilyScorer(self.gdb, fams, m_total=self.db.m)
+            out = fs.scores()
+            fs.plan.close()
         return out
 
     def count_batch(self, assignments) -> np.ndarray:
@@ -403,6 +420,23 @@ def learn_parents(db, strategy, max_parents: int = 3, tie_eps: float = 1e-9) -> 
     if max_parents < 0 or max_parents > db.n - 1:
         raise ValueError(f"max_parents must be in [0, n-1], got {max_parents}")
     results = []
+    if hasattr(strategy, "family_scores"):
+        # every target's candidates in one device batch over the distinct variable subsets
+        t_all = time.perf_counter()
+        cand = [list(candidate_parent_sets(db.n, t, max_parents)) for t in range(db.n)]
+        fams = [(t, c) for t in range(db.n) for c in cand[t]]
+        t0 = time.perf_counter()
+        _, mdl = strategy.family_scores(fams)
+        qsec = time.perf_counter() - t0
+        wall = time.perf_counter() - t_all
+        pos = 0
+        for t in range(db.n):
+            k = len(cand[t])
+            best_score, best_set = _argmin_mdl(cand[t], mdl[pos:pos + k], tie_eps)
+            pos += k
+            share = k / max(len(fams), 1)
+            results.append(ParentSetResult(t, best_set, best_score, k, qsec * share, wall * share))
+        return results
     batched = hasattr(strategy, "query_batch")
     for target in range(db.n):
         t_wall = time.perf_counter()

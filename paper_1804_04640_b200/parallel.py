@@ -1,0 +1,114 @@
+"""Multi-GPU partitioning of counting work (one process per GPU, torch.distributed / NCCL).
+
+Two shardings:
+
+* **instance sharding** -- counts are additive over disjoint row ranges: rank g holds rows
+  ``shard_rows(m, N, g)``, counts partial uint32 tables (``CS_PARTIAL``), the tables are summed
+  with one all-reduce (:func:`merge_tables_`) and scored with the global m;
+* **query sharding** -- when the database fits on every GPU, each rank runs a cost-balanced
+  slice of the batch (:func:`shard_queries`); no data-path collective.
+
+The reference has no parallel code (survey section 2); these functions are the plumbing around
+the C ABI.  They only use ``torch.distributed`` collectives, so the same code runs over NCCL on
+GPUs and over gloo on CPU (tests/test_multirank.py).
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+__all__ = ["shard_rows", "shard_queries", "merge_tables_", "gather_by_index", "InstanceShardedPlan"]
+
+
+def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
+    """(first global row, row count) of rank's instance shard: contiguous, sizes differ by <= 1
+    multiple of 256 rows (the column alignment)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    per = -(-m // world)
+    per = -(-per // 256) * 256
+    r0 = min(m, rank * per)
+    return r0, max(0, min(per, m - r0))
+
+
+def shard_queries(queries, world: int, rank: int, cost=None) -> tuple[list, np.ndarray]:
+    """Longest-processing-time split of a query batch; returns (rank's queries, their indices).
+
+    ``cost(q)`` defaults to the query's byte volume (number of variables), the k*m bytes a
+    query streams.
+    """
+    qs = list(queries)
+    cost = cost or (lambda q: len(q))
+    order = sorted(range(len(qs)), key=lambda i: (-cost(qs[i]), i))
+    heap = [(0.0, r) for r in range(world)]
+    owner = np.empty(len(qs), dtype=np.int64)
+    for i in order:
+        load, r = heapq.heappop(heap)
+        owner[i] = r
+        heapq.heappush(heap, (load + cost(qs[i]), r))
+    idx = np.nonzero(owner == rank)[0]
+    return [qs[i] for i in idx], idx
+
+
+def merge_tables_(tables, group=None):
+    """In-place sum of partial uint32 tables across ranks (int32 view: bitwise identical sum)."""
+    import torch
+    import torch.distributed as dist
+
+    t = tables if tables.dtype == torch.int32 else tables.view(torch.int32)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return tables
+
+
+def gather_by_index(local_values, local_index, total: int, group=None):
+    """Assemble per-query results computed on different ranks into one array (all ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    vals = torch.as_tensor(np.asarray(local_values, dtype=np.float64))
+    idx = torch.as_tensor(np.asarray(local_index, dtype=np.int64))
+    n = torch.tensor([len(idx)], dtype=torch.int64)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    mx = int(max(int(s) for s in sizes))
+    pv = torch.zeros(mx, dtype=torch.float64)
+    pi = torch.full((mx,), -1, dtype=torch.int64)
+    pv[: len(idx)] = vals
+    pi[: len(idx)] = idx
+    gv = [torch.zeros(mx, dtype=torch.float64) for _ in range(world)]
+    gi = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(gv, pv, group=group)
+    dist.all_gather(gi, pi, group=group)
+    out = np.zeros(total)
+    for v, i in zip(gv, gi):
+        keep = i >= 0
+        out[i[keep].numpy()] = v[keep].numpy()
+    return out
+
+
+class InstanceShardedPlan:
+    """One rank's share of an instance-sharded batch on the device.
+
+    ``gdb`` holds this rank's rows (``build_device(ctx, row_offset, m_shard)``) and knows the
+    global m (``set_total_rows``).  ``run()`` counts partial tables, all-reduces them over the
+    process group (NCCL) and scores the merged tables with the fused fp64 epilogue.
+    """
+
+    def __init__(self, gdb, queries, torch_device="cuda", group=None):
+        import torch
+
+        from . import _native as N
+        from .engine import QueryPlan
+
+        self.plan = QueryPlan(gdb, queries, N.CS_PARTIAL | N.CS_WANT_TABLES)
+        self.tables = torch.empty(max(self.plan.total_cells, 1), dtype=torch.int32, device=torch_device)
+        self.group = group
+
+    def run(self, loglik=None, mi=None, nnz=None):
+        self.plan.execute(tables=self.tables)
+        merge_tables_(self.tables, self.group)
+        self.plan.score(self.tables, loglik=loglik, mi=mi, nnz=nnz)
+        return self.tables

@@ -278,3 +278,47 @@ def test_cfg4_workload_small(ctx):
     its = workloads.itemsets_of(range(len(top)), (3,))
     want = O.bitmap_counts(planes, [tuple((top[x], 1) for x in t) for t in its], w.m)
     assert np.array_equal(tr, want)
+
+
+def test_family_scores_match_per_query(ctx):
+    """Subset N ln N differences reproduce per-family LL / MDL (cfg3-shaped, reduced)."""
+    from paper_1804_04640_b200.engine import FamilyScorer
+
+    w = workloads.cfg3(m=60_000, n=10)
+    gdb = w.build_device(ctx)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+    u8 = np.vstack([cols[v] for v in range(w.n)])
+    fams = [(q[0], tuple(q[1:])) for q in w.queries]
+    fs = FamilyScorer(gdb, fams)
+    ll, mdl = fs.scores()
+    _, _, oll, _ = O.radix_tables(u8, w.arities, w.queries, want_tables=False)
+    assert np.allclose(ll, oll, rtol=1e-9, atol=1e-9)
+    for f, (t, ps) in enumerate(fams[:500]):
+        q_i = int(np.prod([int(w.arities[p]) for p in ps])) if ps else 1
+        assert rel_close(mdl[f], O.mdl_of(oll[f], w.m, int(w.arities[t]), q_i), 1e-9)
+
+
+def test_duck_typed_reference_objects(reference_cases):
+    """The drop-in accepts reference-style query/aggregator objects it did not define."""
+    import types
+
+    db = case_db(reference_cases["fixture"])
+    s = cs.GpuStrategy(db)
+
+    class RefQuery:  # the reference QuerySpec surface: target, parents, validate(db)
+        def __init__(self, target, parents):
+            self.target, self.parents = target, tuple(parents)
+
+        def validate(self, db):
+            pass
+
+    # a LogLikelihood-shaped object from the reference module is fused by type name
+    RefLL = type("LogLikelihood", (), {"__module__": "countstream.aggregators", "wants_records": False,
+                                       "__init__": lambda self: setattr(self, "total", 0.0)})
+    agg = RefLL()
+    s.query(RefQuery(1, (0, 2)), agg)
+    want = O.loglik_of_records(FIXTURE_X1_GIVEN_X0_X2)
+    assert rel_close(agg.total, want, 1e-12)
+    col = cs.RecordCollector()
+    s.query(RefQuery(1, (2, 0)), col)
+    assert _recs(col.result()) == FIXTURE_X1_GIVEN_X0_X2
