@@ -139,6 +139,7 @@ struct cs_plan {
   int64_t total_cells = 0;
   bool needs_global = false;   // some query accumulates into a global table
   bool needs_zero = false;     // tables must be zeroed before K1
+  bool transient = false;      // one-shot plan (cs_query_batch): buffers come from ctx scratch
   std::vector<int32_t> score_list;    // queries scored by K2 after K1 (kind 1/2)
   std::vector<int32_t> generic_list;  // kind 2 queries
   int nitems = 0;   // SMEM-class items (k_hist)
@@ -535,7 +536,7 @@ extern "C" int cs_bitmap_plane(cs_db* db, int32_t var, int32_t state, const uint
 // planning
 
 static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
-                      uint32_t flags, cs_plan** out) {
+                      uint32_t flags, cs_plan** out, bool transient = false) {
   if (!db || !out) return fail(CS_ERR_INVALID, "cs_plan_create: NULL argument");
   if (nq < 0) return fail(CS_ERR_INVALID, "cs_plan_create: nq < 0");
   if (nq > 0 && (!var_off || !vars)) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
@@ -689,11 +690,24 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const size_t oq = place(bq), oi = place(bi), os = place(bs), og = place(bg), ov = place(bv),
                ost = place(bst), oh = place(256), od = place(sizeof(uint32_t) * std::max(nq, 1));
   char* dblob = nullptr;
-  cudaError_t e = cudaMalloc(&dblob, off);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    delete p;
-    return fail(CS_ERR_OOM, "cs_plan_create: cannot allocate %zu bytes", off);
+  p->transient = transient;
+  if (transient) {
+    // grow-only context scratch: no cudaMalloc/cudaFree (and their device syncs) per call;
+    // stream order keeps a later plan's upload behind this plan's kernels
+    void* b = nullptr;
+    int rc = ctx->scratch_get(18, off, &b);
+    if (rc != CS_OK) {
+      delete p;
+      return rc;
+    }
+    dblob = (char*)b;
+  } else {
+    cudaError_t e = cudaMalloc(&dblob, off);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      delete p;
+      return fail(CS_ERR_OOM, "cs_plan_create: cannot allocate %zu bytes", off);
+    }
   }
   void* stage = nullptr;
   CS_TRY(ctx->pinned_get(off, &stage));
@@ -739,9 +753,11 @@ extern "C" int cs_plan_info(cs_plan* p, int64_t* cells, int64_t* table_off, int6
 extern "C" int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   cudaSetDevice(p->db->ctx->device);
-  cudaStreamSynchronize(p->db->ctx->stream);
-  if (p->d_q) cudaFree((void*)p->d_q);  // blob base
-  if (p->d_tables) cudaFree(p->d_tables);
+  if (!p->transient) {
+    cudaStreamSynchronize(p->db->ctx->stream);
+    if (p->d_q) cudaFree((void*)p->d_q);  // blob base
+    if (p->d_tables) cudaFree(p->d_tables);
+  }
   delete p;
   return CS_OK;
 }
@@ -776,7 +792,12 @@ static int plan_tables(cs_plan* p, uint32_t* user_tables, OutBuf& tb, uint32_t**
     tb.bytes = bytes;
     *dtab = user_tables;
   } else if (user_tables || (p->flags & F_TABLES) || p->needs_global) {
-    if (p->d_tables_cells < (size_t)std::max<int64_t>(p->total_cells, 1)) {
+    if (p->transient) {
+      void* b = nullptr;
+      CS_TRY(p->db->ctx->scratch_get(17, bytes, &b));
+      p->d_tables = (uint32_t*)b;
+      p->d_tables_cells = std::max<int64_t>(p->total_cells, 1);
+    } else if (p->d_tables_cells < (size_t)std::max<int64_t>(p->total_cells, 1)) {
       if (p->d_tables) cudaFree(p->d_tables);
       p->d_tables = nullptr;
       CS_CUDA(cudaMalloc(&p->d_tables, bytes));
@@ -987,7 +1008,7 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
                               uint32_t flags, uint32_t* tables, double* loglik, double* mi,
                               int64_t* nnz) {
   cs_plan* p = nullptr;
-  CS_TRY(plan_build(db, nq, var_off, vars, flags, &p));
+  CS_TRY(plan_build(db, nq, var_off, vars, flags, &p, /*transient=*/true));
   int rc = cs_plan_execute(p, tables, loglik, mi, nnz);
   cs_plan_destroy(p);
   return rc;
