@@ -167,6 +167,9 @@ def workload(config: str, world: int, rank: int, nq_override):
         w = W.cfg1(nq=(nq_override or 1000) * world)
     elif config == "cfg2":
         w = W.cfg2(nq=(nq_override or 10_000) * world)
+        kf = os.environ.get("CS_BENCH_KFILTER")  # diagnostic: only queries with k variables
+        if kf:
+            w.queries = [q for q in w.queries if len(q) == int(kf)]
     elif config == "cfg3":
         w = W.cfg3()
         if nq_override:

@@ -69,6 +69,24 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
+// K1 variants: kHist[k-1][path][nibble layout] (nullptr where a path needs fewer digits)
+using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32_t*, double*, double*,
+                        int64_t*, uint32_t, double);
+#define CS_HK(K)                                                                           \
+  {{k_hist<K, P_LANE16, false>, k_hist<K, P_LANE16, true>},                                \
+   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, false> : nullptr,                           \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, true> : nullptr},                           \
+   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, false> : nullptr,                           \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, true> : nullptr},                           \
+   {k_hist<K, P_ROWS, false>, nullptr}}
+static const HistFn kHist[CS_MAXK][4][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
+                                            CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
+#undef CS_HK
+
+static int hist_path(const QDesc& d) {
+  return d.pack == 4 ? P_PACK4 : (d.pack == 2 ? P_PACK2 : (d.mode == 0 ? P_LANE16 : P_ROWS));
+}
+
 // ------------------------------------------------------------------------------------------
 // handles
 
@@ -79,8 +97,7 @@ struct cs_ctx {
   int num_sms = 0;
   int hist_smem = 0;      // dynamic SMEM bytes per K1 CTA
   int hist_ctas = 0;      // resident K1 CTAs (persistent grid)
-  int hist_threads = 768;
-  int hist_cfg = 0;
+  int hist_threads = CS_HIST_THREADS;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the last K1 launch
   bool ev_valid = false;
   int64_t launches = 0;
@@ -122,6 +139,8 @@ struct cs_db {
   int32_t n = 0;
   int64_t m = 0, ld = 0, m_total = 0;
   uint8_t* cols = nullptr;
+  uint8_t* nib = nullptr;  // 4-bit copy (all arities <= 16), ldn bytes per column
+  int64_t ldn = 0;
   int32_t* d_arity = nullptr;
   std::vector<int32_t> arity;
   // bitmap index
@@ -142,6 +161,10 @@ struct cs_plan {
   bool transient = false;      // one-shot plan (cs_query_batch): buffers come from ctx scratch
   std::vector<int32_t> score_list;    // queries scored by K2 after K1 (kind 1/2)
   std::vector<int32_t> generic_list;  // kind 2 queries
+  struct Group {
+    int key, first, count;
+  };
+  std::vector<Group> groups;  // SMEM-class item groups, one K1 launch each
   int nitems = 0;   // SMEM-class items (k_hist)
   int ngitems = 0;  // global-class items (k_hist_global), stored after the SMEM items
   // device
@@ -194,34 +217,18 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   CS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
-  // K1 shape (CS_HIST_CFG): "wide" = one 768-thread CTA per SM with ~220 KB SMEM (32
-  // conflict-free replicas up to C = 1760 cells); "widepf" = same + software prefetch for
-  // K <= 4; "full" = one 1024-thread CTA per SM (64 registers); "pair" = two 384-thread CTAs
-  // per SM with 104 KB each.
-  // Default "full": measured fastest on cfg2 (profiles/README.md, round 1).
-  const char* cfg = getenv("CS_HIST_CFG");
-  c->hist_cfg = 2;
-  if (cfg && strcmp(cfg, "wide") == 0) c->hist_cfg = 0;
-  if (cfg && strcmp(cfg, "widepf") == 0) c->hist_cfg = 1;
-  if (cfg && strcmp(cfg, "pair") == 0) c->hist_cfg = 3;
-  static const int kThreads[4] = {768, 768, 1024, 384};
-  c->hist_threads = kThreads[c->hist_cfg];
+  // K1: one 1024-thread CTA per SM with ~220 KB of dynamic SMEM (32 conflict-free replicas up
+  // to C = 1760 cells, or a cp.async ring for narrow queries); measured best on cfg2
+  // (profiles/README.md).  The attribute is per function (process-wide): raise it once.
   const int smem_cap = (int)prop.sharedMemPerBlockOptin - (int)sizeof(ScoreSmem) - 1024;
-  int kb = env_int("CS_HIST_SMEM_KB", c->hist_cfg == 3 ? 104 : 220);
-  c->hist_smem = std::min(kb * 1024, smem_cap);
-  // the attribute is per function (process-wide): raise it to the device maximum once so
-  // contexts with different budgets can coexist
-  CS_CUDA(cudaFuncSetAttribute(k_hist<768, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-  CS_CUDA(cudaFuncSetAttribute(k_hist<768, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-  CS_CUDA(cudaFuncSetAttribute(k_hist<1024, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-  CS_CUDA(cudaFuncSetAttribute(k_hist<384, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+  c->hist_smem = std::min(env_int("CS_HIST_SMEM_KB", 220) * 1024, smem_cap);
+  for (auto& a : kHist)
+    for (auto& b : a)
+      for (HistFn f : b)
+        if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
   int per_sm = 0;
-  switch (c->hist_cfg) {
-    case 0: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<768, 1, false>, 768, c->hist_smem)); break;
-    case 1: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<768, 1, true>, 768, c->hist_smem)); break;
-    case 2: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<1024, 1, false>, 1024, c->hist_smem)); break;
-    default: CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist<384, 2, false>, 384, c->hist_smem)); break;
-  }
+  CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kHist[7][0][0], CS_HIST_THREADS,
+                                                        c->hist_smem));
   if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
@@ -327,7 +334,32 @@ static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, c
                           ctx->stream));
   // zero padding (and everything: generated DBs fill columns later)
   CS_CUDA(cudaMemsetAsync(db->cols, 0, (size_t)n * db->ld, ctx->stream));
+  // 4-bit copy for the bandwidth-bound histogram kernels when every arity fits a nibble
+  bool small = env_int("CS_NIBBLE", 1) != 0;
+  for (int i = 0; i < n && small; ++i) small = arities[i] <= 16;
+  if (small) {
+    db->ldn = round_up((m + 1) / 2, 256);
+    if (cudaMalloc(&db->nib, (size_t)n * db->ldn) != cudaSuccess) {
+      cudaGetLastError();  // not enough memory: the kernels read the uint8 columns instead
+      db->nib = nullptr;
+      db->ldn = 0;
+    } else {
+      CS_CUDA(cudaMemsetAsync(db->nib, 0, (size_t)n * db->ldn, ctx->stream));
+    }
+  }
   *out = db;
+  return CS_OK;
+}
+
+// (re)pack columns [var0, var0 + nvars) into the 4-bit copy
+static int db_pack(cs_db* db, int32_t var0, int32_t nvars) {
+  if (!db->nib || nvars <= 0) return CS_OK;
+  cs_ctx* ctx = db->ctx;
+  const int64_t words = (db->m + 7) >> 3;
+  dim3 grid((unsigned)std::min<int64_t>((words + 255) / 256, 2048), (unsigned)std::min(nvars, 1024));
+  k_pack4<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, db->nib, db->ldn, db->m, var0, nvars);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
   return CS_OK;
 }
 
@@ -369,6 +401,7 @@ extern "C" int cs_db_create(cs_ctx* ctx, const uint8_t* cols, int32_t n, int64_t
       return rc;
     }
   }
+  CS_TRY(db_pack(db, 0, n));
   *out = db;
   return CS_OK;
 }
@@ -418,6 +451,7 @@ extern "C" int cs_db_generate(cs_db* db, int32_t var, uint64_t seed, int64_t row
                                             r - 1);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
+  CS_TRY(db_pack(db, var, 1));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(blob);
   return CS_OK;
@@ -428,6 +462,7 @@ extern "C" int cs_db_destroy(cs_db* db) {
   cudaSetDevice(db->ctx->device);
   cudaStreamSynchronize(db->ctx->stream);
   if (db->cols) cudaFree(db->cols);
+  if (db->nib) cudaFree(db->nib);
   if (db->d_arity) cudaFree(db->d_arity);
   if (db->planes) cudaFree(db->planes);
   delete db;
@@ -605,8 +640,17 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         gstride.push_back((uint32_t)s);
         s *= db->arity[vars[b + i]];
       }
+    } else if (c <= 6 && c * c * c * c * 32 <= smem_words && env_int("CS_PACK", 1)) {
+      d.kind = 0;  // 4 rows per atomic (hist_smem_packed<K, 4>)
+      d.pack = 4;
+      d.rlog = 5;
+    } else if (c <= 41 && c * c * 32 <= smem_words && env_int("CS_PACK", 1)) {
+      d.kind = 0;  // 2 rows per atomic (hist_smem_packed<K, 2>)
+      d.pack = 2;
+      d.rlog = 5;
     } else if (c <= smem_words) {
       d.kind = 0;
+      d.pack = 1;
       // replicas: as many as fit (<= 32; R = 32 makes every ATOMS wavefront conflict-free).
       // When C*R*4 <= 64 KB the byte offsets fit 16-bit SIMD lanes (mode 0, hist_smem_lane16).
       int rl = 0;
@@ -616,6 +660,40 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     } else {
       d.kind = 1;
       d.mode = c <= 65536 ? 1 : 2;
+    }
+    if (d.kind == 0) {
+      // cp.async ring for the row stream: up to 4 stages in the SMEM left after the table
+      // (K <= 4 only: higher K keeps its SMEM for conflict-free replicas instead)
+      const int64_t smem_bytes = (int64_t)ctx->hist_smem;
+      const int64_t per_stage = (int64_t)k * 16 * ctx->hist_threads;
+      auto table_bytes = [&](const QDesc& x) {
+        int64_t ct = x.cells;
+        for (int i = 1; i < x.pack; ++i) ct *= x.cells;
+        return round_up((ct << x.rlog) * 4, 128);
+      };
+      if (k <= 4 && env_int("CS_STAGES", 1)) {
+        // shrink packing first if it is what keeps the ring from fitting 3 stages
+        while (d.pack > 1 && table_bytes(d) + 3 * per_stage > smem_bytes) {
+          d.pack = d.pack == 4 ? 2 : 1;
+          if (d.pack == 1) {
+            int rl = 0;
+            while (rl < 5 && (c << (rl + 1)) <= smem_words) ++rl;
+            d.rlog = rl;
+            d.mode = (c << rl) <= 16384 ? 0 : (c <= 65536 ? 1 : 2);
+          }
+        }
+        const int64_t left = smem_bytes - table_bytes(d);
+        const int st = (int)std::min<int64_t>(4, left / std::max<int64_t>(per_stage, 1));
+        if (st >= 3 && (d.pack > 1 || d.mode == 0)) {
+          d.stages = st;
+          d.stage_off = (uint32_t)table_bytes(d);
+        }
+      }
+    }
+    if (d.kind == 0 && db->nib && (d.pack > 1 || d.mode == 0) && env_int("CS_NIBBLE", 1)) {
+      d.nib = 1;
+      d.base = db->nib;
+      for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
     }
     p->hq[q] = d;
     p->cells[q] = c;
@@ -663,15 +741,37 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // longest-processing-time-first order for the persistent CTAs
   std::vector<int> order(items.size());
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  // SMEM-class items first, then global-class items (each list in LPT order)
+  // Segment-major (CS_SEG_ORDER=1, default): all items of row segment 0 first, then 1, ...;
+  // LPT within a segment.  Concurrently running CTAs then share one row window of the
+  // columns, which stays L2-resident (the L2 is split per die, so a 100 MB database does not).
+  const bool seg_major = env_int("CS_SEG_ORDER", 1) != 0;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    if (seg_major && items[a].seg != items[b].seg) return items[a].seg < items[b].seg;
+    return cost[a] > cost[b];
+  });
+  // SMEM-class items grouped by K1 variant (k, path, layout), groups by descending total cost,
+  // LPT order inside a group; then the global-class items.
+  std::map<int, std::vector<int>> groups;  // key = (k-1)*8 + path*2 + nib
+  std::map<int, double> gcost;
+  for (size_t i = 0; i < order.size(); ++i) {
+    const QDesc& d = p->hq[items[order[i]].q];
+    if (d.kind != 0) continue;
+    const int key = (d.k - 1) * 8 + hist_path(d) * 2 + d.nib;
+    groups[key].push_back(order[i]);
+    gcost[key] += cost[order[i]];
+  }
+  std::vector<int> keys;
+  for (auto& kv : groups) keys.push_back(kv.first);
+  std::stable_sort(keys.begin(), keys.end(), [&](int a, int b) { return gcost[a] > gcost[b]; });
   std::vector<WItem> sorted;
   sorted.reserve(items.size());
-  for (int pass = 0; pass < 2; ++pass)
-    for (size_t i = 0; i < order.size(); ++i)
-      if ((p->hq[items[order[i]].q].kind == 0) == (pass == 0)) sorted.push_back(items[order[i]]);
-  p->nitems = 0;
-  for (const WItem& w : sorted) p->nitems += p->hq[w.q].kind == 0;
+  for (int key : keys) {
+    p->groups.push_back({key, (int)sorted.size(), (int)groups[key].size()});
+    for (int i : groups[key]) sorted.push_back(items[i]);
+  }
+  p->nitems = (int)sorted.size();
+  for (size_t i = 0; i < order.size(); ++i)
+    if (p->hq[items[order[i]].q].kind == 1) sorted.push_back(items[order[i]]);
   p->ngitems = (int)sorted.size() - p->nitems;
   // upload descriptors (one blob through pinned staging)
   CS_CUDA(cudaSetDevice(ctx->device));
@@ -688,7 +788,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     return o;
   };
   const size_t oq = place(bq), oi = place(bi), os = place(bs), og = place(bg), ov = place(bv),
-               ost = place(bst), oh = place(256), od = place(sizeof(uint32_t) * std::max(nq, 1));
+               ost = place(bst), oh = place(1024), od = place(sizeof(uint32_t) * std::max(nq, 1));
   char* dblob = nullptr;
   p->transient = transient;
   if (transient) {
@@ -868,7 +968,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   }
   if (p->needs_zero && dtab)
     CS_CUDA(cudaMemsetAsync(dtab, 0, sizeof(uint32_t) * p->total_cells, ctx->stream));
-  CS_CUDA(cudaMemsetAsync(p->d_head, 0, 256, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(p->d_head, 0, 1024, ctx->stream));
   CS_CUDA(cudaMemsetAsync(p->d_done, 0, sizeof(uint32_t) * p->nq, ctx->stream));
   const double m_total = (double)db->m_total;
   // ev0/ev1 bracket the whole histogram phase (K1 global + K1 SMEM + K1g) on this stream
@@ -881,20 +981,18 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     CS_CUDA(cudaGetLastError());
   }
   if (p->nitems > 0) {
-    const int grid = std::min(ctx->hist_ctas, p->nitems);
-#define CS_LAUNCH_HIST(T, B, PF)                                                              \
-  k_hist<T, B, PF><<<grid, T, ctx->hist_smem, ctx->stream>>>(                                 \
-      p->d_q, p->d_items, p->nitems, p->d_head, dtab, p->d_done, (double*)lb.dev, (double*)mb.dev, \
-      (int64_t*)nb.dev, flags, m_total)
-    switch (ctx->hist_cfg) {
-      case 0: CS_LAUNCH_HIST(768, 1, false); break;
-      case 1: CS_LAUNCH_HIST(768, 1, true); break;
-      case 2: CS_LAUNCH_HIST(1024, 1, false); break;
-      default: CS_LAUNCH_HIST(384, 2, false); break;
+    for (size_t g = 0; g < p->groups.size(); ++g) {
+      const auto& G = p->groups[g];
+      const int k = G.key / 8 + 1, path = (G.key % 8) / 2, nib = G.key % 2;
+      HistFn f = kHist[k - 1][path][nib];
+      if (!f) return fail(CS_ERR_INVALID, "internal: no K1 variant for k=%d path=%d", k, path);
+      const int grid = std::min(ctx->hist_ctas, G.count);
+      f<<<grid, CS_HIST_THREADS, ctx->hist_smem, ctx->stream>>>(
+          p->d_q, p->d_items + G.first, G.count, p->d_head + 2 + (int)g, dtab, p->d_done,
+          (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev, flags, m_total);
+      ctx->launches++;
+      CS_CUDA(cudaGetLastError());
     }
-#undef CS_LAUNCH_HIST
-    ctx->launches++;
-    CS_CUDA(cudaGetLastError());
   }
   if (!p->generic_list.empty()) {
     dim3 grid((unsigned)std::min<int64_t>((db->m + 255) / 256, 1024), (unsigned)p->generic_list.size());

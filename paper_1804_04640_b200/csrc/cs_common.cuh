@@ -5,6 +5,10 @@
 //             database.py:53, narrowed to uint8), ld = round_up(m, 256) so every column
 //             starts 256-B aligned and every 16-row vector load is aligned and in bounds.
 //             Bytes past m are zero and never counted.
+//   nibbles : 4-bit copy of the columns when every arity <= 16 (n x ldn bytes, ldn =
+//             round_up(ceil(m/2), 256)); byte j holds row 2j (low nibble) and row 2j+1 (high
+//             nibble).  The histogram kernels are L2/HBM-bandwidth bound, so they read this copy:
+//             half the bytes per row.
 //   planes  : optional bit planes, one per (variable, state), `words` uint32 per plane,
 //             bit t%32 of word t/32 = record t (reference bitmap.py:29-31 little-endian).
 #pragma once
@@ -31,7 +35,10 @@ struct __align__(16) QDesc {
   int32_t nseg;                 // row segments this query is split into
   int32_t kind;                 // 0 SMEM class, 1 global-atomic class, 2 generic (k > CS_MAXK)
   int32_t var_base;             // generic class: offset into the plan's var list
-  int32_t pad_[1];
+  int32_t pack;                 // SMEM class: rows per atomic (1, or 2 / 4 packed tuples)
+  int32_t stages;               // SMEM class: cp.async prefetch ring depth (0 = direct loads)
+  uint32_t stage_off;           // SMEM class: byte offset of the ring in dynamic SMEM
+  int32_t nib;                  // 1: columns read from the 4-bit (nibble) copy, 32 rows / 16 B
 };
 
 // One unit of work: rows [r0, r1) of query q.

@@ -28,6 +28,20 @@ __device__ __forceinline__ uint4 ldg_stream16(const uint8_t* p) {
   return r;
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t smem_addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_addr));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t word_of(const uint4& w, int j) {
   return j == 0 ? w.x : (j == 1 ? w.y : (j == 2 ? w.z : w.w));
 }
@@ -123,6 +137,66 @@ __device__ void score_table(CellFn cell, uint32_t C, int rt, double m_total, uin
   }
 }
 
+// Cell-parallel scoring from a compact SMEM table (tab[c] = N of cell c): every thread takes
+// cells, not configurations, so small tables with few configurations still use the whole CTA.
+// nij: SMEM scratch of C / rt words (parent-configuration totals).  Same sums as score_table.
+__device__ void score_cells(const uint32_t* tab, uint32_t C, int rt, uint32_t* nij, double m_total,
+                            uint32_t flags, int q, double* ll_out, double* mi_out, int64_t* nnz_out,
+                            ScoreSmem& ss) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const bool want_mi = (flags & F_MI) != 0;
+  const bool nlogn = (flags & F_NLOGN) != 0;
+  const uint32_t J = C / (uint32_t)rt;
+  const bool need_nij = want_mi || ((flags & F_LOGLIK) && !nlogn);
+  if (want_mi) {
+    for (int k = tid; k < rt; k += nt) ss.marg[k] = 0ull;
+  }
+  if (need_nij) {
+    for (uint32_t j = tid; j < J; j += nt) {
+      uint32_t sum = 0;
+      for (int k = 0; k < rt; ++k) sum += tab[j * (uint32_t)rt + k];
+      nij[j] = sum;
+    }
+  }
+  __syncthreads();
+  if (want_mi) {
+    for (uint32_t c = tid; c < C; c += nt) {
+      const uint32_t v = tab[c];
+      if (v) atomicAdd(&ss.marg[c % (uint32_t)rt], (unsigned long long)v);
+    }
+    __syncthreads();
+  }
+  double ll = 0.0, mi = 0.0;
+  unsigned long long nz = 0;
+  for (uint32_t c = tid; c < C; c += nt) {
+    const uint32_t n = tab[c];
+    if (!n) continue;
+    const double x = (double)n;
+    ++nz;
+    if (nlogn) {
+      ll += x * log(x);
+    } else if (flags & (F_LOGLIK | F_MI)) {
+      const double dnij = (double)nij[c / (uint32_t)rt];
+      ll += x * log(x / dnij);
+      if (want_mi) mi += x * log((x * m_total) / (dnij * (double)ss.marg[c % (uint32_t)rt]));
+    }
+  }
+  const double tll = block_sum(ll, ss.red);
+  const double tmi = want_mi ? block_sum(mi, ss.red) : 0.0;
+  const unsigned long long tnz = block_sum_u64(nz, ss.redu);
+  if (tid == 0) {
+    if (ll_out) ll_out[q] = tll;
+    if (mi_out) mi_out[q] = want_mi ? tmi / m_total : 0.0;
+    if (nnz_out) nnz_out[q] = (int64_t)tnz;
+  }
+}
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 // ------------------------------------------------------------------------------------------
 // K1 inner loop: count rows [r0, r1) of one query.
 //
@@ -143,6 +217,51 @@ __device__ void score_table(CellFn cell, uint32_t C, int rt, double m_total, uin
 // read zero padding; they are counted into cell 0 of the thread's replica and subtracted
 // once after the loop (no per-row tail predicate).
 
+// Staged (cp.async) row loop shared by the SMEM-class counters: each thread keeps a private
+// ring of S slots (K x 16 B each) in shared memory and issues the 16-byte copies of its vector
+// S-1 iterations ahead (cp.async.cg: L2 -> SMEM, no registers held while in flight), then reads
+// its own slot back with LDS.128.  Only the issuing thread reads a slot, so no barrier is
+// needed; a slot is refilled one iteration after its values were consumed.
+template <int K, int S, class Count>
+__device__ __forceinline__ void staged_rows(const uint8_t* rowp, const uint32_t (&co)[K], int64_t nvec,
+                                            uint32_t ring, Count count) {
+  const int64_t bd = blockDim.x;
+  const uint32_t me = ring + 16u * threadIdx.x;
+  auto slot = [&](int s, int v) -> uint32_t { return me + (uint32_t)((s * K + v) * bd) * 16u; };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    const int64_t vi = threadIdx.x + s * bd;
+    if (vi < nvec) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) cp_async16(slot(s, v), rowp + (vi << 4) + ((uint64_t)co[v] << 8));
+    }
+    cp_async_commit();
+  }
+  int s_rd = 0, s_wr = S - 1;
+  for (int64_t vi = threadIdx.x; vi < nvec; vi += bd) {
+    const int64_t vn = vi + (S - 1) * bd;
+    if (vn < nvec) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) cp_async16(slot(s_wr, v), rowp + (vn << 4) + ((uint64_t)co[v] << 8));
+    }
+    cp_async_commit();
+    cp_async_wait<S - 1>();
+    uint32_t x[K][4];
+#pragma unroll
+    for (int v = 0; v < K; ++v) {
+      const uint4 t = lds128(slot(s_rd, v));
+      x[v][0] = t.x;
+      x[v][1] = t.y;
+      x[v][2] = t.z;
+      x[v][3] = t.w;
+    }
+    count(x);
+    s_rd = (s_rd + 1 == S) ? 0 : s_rd + 1;
+    s_wr = (s_wr + 1 == S) ? 0 : s_wr + 1;
+  }
+  cp_async_wait<0>();
+}
+
 template <int K>
 __device__ __forceinline__ void load_vec16(uint32_t (&x)[K][4], const uint8_t* p,
                                            const uint32_t (&co)[K]) {
@@ -156,38 +275,37 @@ __device__ __forceinline__ void load_vec16(uint32_t (&x)[K][4], const uint8_t* p
   }
 }
 
-template <int K>
-__device__ __forceinline__ void count_vec16(const uint32_t (&x)[K][4], const uint32_t (&st)[K],
-                                            int nbyte, uint32_t scale, uint32_t rep_pair,
-                                            char* shb) {
+// Word views of one loaded 16-byte vector per column: 4 words of 4 byte-lane rows (uint8
+// layout), or 8 words (nibble layout: low nibbles = even rows, high nibbles = odd rows, each
+// widened to byte lanes with one LOP3 / SHF+LOP3).  Row order inside a vector is irrelevant
+// to counting.
+template <int K, bool NIB, class WordFn>
+__device__ __forceinline__ void for_words(const uint32_t (&x)[K][4], WordFn f) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    uint32_t a8 = x[0][j];
+    if (!NIB) {
+      uint32_t w[K];
 #pragma unroll
-    for (int v = 1; v < K; ++v)
-      if (v < nbyte) a8 += x[v][j] * st[v];
-    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+      for (int v = 0; v < K; ++v) w[v] = x[v][j];
+      f(w);
+    } else {
+      uint32_t w0[K], w1[K];
 #pragma unroll
-    for (int v = 1; v < K; ++v) {
-      if (v >= nbyte) {
-        lo += __byte_perm(x[v][j], 0u, 0x4140) * st[v];
-        hi += __byte_perm(x[v][j], 0u, 0x4342) * st[v];
+      for (int v = 0; v < K; ++v) {
+        w0[v] = x[v][j] & 0x0f0f0f0fu;
+        w1[v] = (x[v][j] >> 4) & 0x0f0f0f0fu;
       }
+      f(w0);
+      f(w1);
     }
-    lo = lo * scale + rep_pair;
-    hi = hi * scale + rep_pair;
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
   }
 }
 
-template <int K, bool PF>
+template <int K, bool NIB>
 __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int64_t r1,
                                                  uint32_t* sh) {
-  const uint8_t* rowp = q.base + r0;
+  constexpr int RPV = NIB ? 32 : 16;  // rows per 16-byte vector
+  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -201,31 +319,93 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
   const uint32_t rep_pair = rep4 | (rep4 << 16);
   char* shb = reinterpret_cast<char*>(sh);
   const int64_t nrows = r1 - r0;
-  const int64_t nvec = (nrows + 15) >> 4;
-  const int64_t bd = blockDim.x;
-  int64_t vi = threadIdx.x;
-  if (PF && K <= 4) {
-    // ping-pong: vector i+1's K loads are in flight while vector i is counted
-    uint32_t a[K][4], b[K][4];
-    if (vi < nvec) load_vec16<K>(a, rowp + (vi << 4), co);
-    for (; vi < nvec; vi += 2 * bd) {
-      const bool hb = vi + bd < nvec;
-      if (hb) load_vec16<K>(b, rowp + ((vi + bd) << 4), co);
-      count_vec16<K>(a, st, nbyte, scale, rep_pair, shb);
-      if (!hb) break;
-      if (vi + 2 * bd < nvec) load_vec16<K>(a, rowp + ((vi + 2 * bd) << 4), co);
-      count_vec16<K>(b, st, nbyte, scale, rep_pair, shb);
+  const int64_t nvec = (nrows + RPV - 1) / RPV;
+  auto word = [&](const uint32_t (&w)[K]) {
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K; ++v)
+      if (v < nbyte) a8 += w[v] * st[v];
+    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K; ++v) {
+      if (v >= nbyte) {
+        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      }
     }
+    lo = lo * scale + rep_pair;
+    hi = hi * scale + rep_pair;
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
+  };
+  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+  if (q.stages >= 3) {
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
   } else {
-    for (; vi < nvec; vi += bd) {
+    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
       uint32_t a[K][4];
       load_vec16<K>(a, rowp + (vi << 4), co);
-      count_vec16<K>(a, st, nbyte, scale, rep_pair, shb);
+      cnt(a);
     }
   }
-  const int64_t pad = (nvec << 4) - nrows;  // padding rows counted into cell 0
-  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % bd))
+  const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
+}
+
+// SMEM class, tiny tables (C <= 41): PACK consecutive rows share one atomic.  The byte lanes
+// of a word hold 4 rows' joint indices (< C <= 255); one IDP4A per tuple folds them into the
+// tuple index  b0 + C b1 (+ C^2 b2 + C^3 b3)  of a C^PACK-cell table (32 replicas), so the
+// SMEM atomic traffic drops PACK-fold; the epilogue marginalises the tuple table back to the
+// C cells.  Padding rows (zeros) are subtracted from cell 0 in the epilogue.
+template <int K, int PACK, bool NIB>
+__device__ __forceinline__ void hist_smem_packed(const QDesc& q, int64_t r0, int64_t r1,
+                                                 uint32_t* sh) {
+  constexpr int RPV = NIB ? 32 : 16;
+  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  uint32_t co[K], st[K];
+#pragma unroll
+  for (int v = 0; v < K; ++v) {
+    co[v] = q.coff[v];
+    st[v] = q.stride[v];
+  }
+  const uint32_t C = q.cells;
+  const uint32_t m2a = 1u | (C << 8), m2b = (1u << 16) | (C << 24);
+  const uint32_t m4 = 1u | (C << 8) | ((C * C) << 16) | ((C * C * C) << 24);
+  const int rlog = q.rlog;
+  const uint32_t scale = 4u << rlog;
+  const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
+  char* shb = reinterpret_cast<char*>(sh) + rep4;
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + RPV - 1) / RPV;
+  auto word = [&](const uint32_t (&w)[K]) {
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K; ++v) a8 += w[v] * st[v];
+    if (PACK == 4) {
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, m4, 0u) * scale), 1u);
+    } else {
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, m2a, 0u) * scale), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, m2b, 0u) * scale), 1u);
+    }
+  };
+  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+  if (q.stages >= 3) {
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
+    return;
+  }
+  for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+    uint32_t x[K][4];
+    load_vec16<K>(x, rowp + (vi << 4), co);
+    cnt(x);
+  }
 }
 
 // Other classes: scalar 32-bit index per row.
@@ -298,18 +478,12 @@ __device__ __forceinline__ void hist_rows(const QDesc& q, int64_t r0, int64_t r1
     atomicSub(base + (SMEM ? rep : 0u), (uint32_t)pad);
 }
 
-template <bool SMEM, bool PF = false>
-__device__ __forceinline__ void dispatch_rows(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
-                                              uint32_t* gtab) {
-#define CS_CASE_K(KK)                                                        \
-  case KK:                                                                   \
-    if (SMEM) {                                                              \
-      if (q.mode == 0) hist_smem_lane16<KK, PF>(q, r0, r1, sh);              \
-      else hist_rows<KK, 1, true>(q, r0, r1, sh, gtab);                      \
-    } else {                                                                 \
-      if (q.mode <= 1) hist_rows<KK, 1, false>(q, r0, r1, sh, gtab);         \
-      else hist_rows<KK, 2, false>(q, r0, r1, sh, gtab);                     \
-    }                                                                        \
+__device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0, int64_t r1,
+                                                     uint32_t* gtab) {
+#define CS_CASE_K(KK)                                                  \
+  case KK:                                                             \
+    if (q.mode <= 1) hist_rows<KK, 1, false>(q, r0, r1, nullptr, gtab); \
+    else hist_rows<KK, 2, false>(q, r0, r1, nullptr, gtab);            \
     break;
   switch (q.k) {
     CS_CASE_K(1)
@@ -330,8 +504,17 @@ __device__ __forceinline__ void dispatch_rows(const QDesc& q, int64_t r0, int64_
 // *head.  kind 0 (SMEM) items finish with the fused epilogue: a single-segment query writes
 // its table and scores straight from SMEM; a multi-segment query adds its partial table into
 // global memory and the last segment to arrive (done[] counter) scores the merged table.
-template <int THREADS, int MINB, bool PF>
-__global__ void __launch_bounds__(THREADS, MINB)
+// Persistent K1, one instantiation per (K variables, counting path, column layout), so every
+// variant gets its own register allocation (a single kernel carrying all paths spills).
+// Items of the group are sorted by descending cost on the host; CTAs pull them from *head.
+// An SMEM item finishes with the fused epilogue: a single-segment query writes its table and
+// scores straight from SMEM; a multi-segment query adds its partial table into global memory
+// and the last segment to arrive (done counter) scores the merged table.
+enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3 };
+constexpr int CS_HIST_THREADS = 1024;
+
+template <int K, int PATH, bool NIB>
+__global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     k_hist(const QDesc* __restrict__ qd, const WItem* __restrict__ items, int nitems,
            int* __restrict__ head, uint32_t* tables, uint32_t* __restrict__ done, double* ll_out,
            double* mi_out, int64_t* nnz_out, uint32_t flags, double m_total) {
@@ -339,7 +522,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
   __shared__ QDesc s_q;
   __shared__ int s_item, s_last;
   __shared__ ScoreSmem ss;
+  __shared__ uint32_t s_marg[64];  // marginal counts of packed-tuple tables (C <= 41)
+  __shared__ uint32_t s_nij[64];   // their configuration totals
   const bool want_score = !(flags & F_PARTIAL) && (flags & (F_LOGLIK | F_MI | F_NNZ));
+  constexpr int pack = PATH == P_PACK4 ? 4 : (PATH == P_PACK2 ? 2 : 1);
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(head, 1);
     __syncthreads();
@@ -354,23 +540,62 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int rl = q.rlog;
     const uint32_t R = 1u << rl;
     const uint32_t C = q.cells;
-    const uint32_t nw = C << rl;
+    uint32_t ct = C;  // cells of the SMEM table (C^pack for packed tuples)
+    for (int i = 1; i < pack; ++i) ct *= C;
+    const uint32_t nw = ct << rl;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
+    if (threadIdx.x < 64) s_marg[threadIdx.x] = 0u;
     __syncthreads();
-    dispatch_rows<true, PF>(q, wi.r0, wi.r1, sh, nullptr);
+    if (PATH == P_LANE16) hist_smem_lane16<K, NIB>(q, wi.r0, wi.r1, sh);
+    else if (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
+    else if (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
+    else hist_rows<K, 1, true>(q, wi.r0, wi.r1, sh, nullptr);
     __syncthreads();
-    auto cell = [&](uint32_t c) -> uint32_t {
+    auto rep_sum = [&](uint32_t c) -> uint32_t {
       uint32_t s = 0;
       for (uint32_t r = 0; r < R; ++r) s += sh[(c << rl) | ((r + c) & (R - 1u))];
       return s;
     };
+    if (pack > 1) {
+      // marginalise the tuple table: every digit position of a tuple is one row
+      for (uint32_t t = threadIdx.x; t < ct; t += blockDim.x) {
+        const uint32_t v = rep_sum(t);
+        if (v) {
+          uint32_t x = t;
+          for (int j = 0; j < pack; ++j) {
+            atomicAdd(&s_marg[x % C], v);
+            x /= C;
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int64_t nrows = wi.r1 - wi.r0, rpv = NIB ? 32 : 16;
+        s_marg[0] -= (uint32_t)((nrows + rpv - 1) / rpv * rpv - nrows);  // zero padding rows
+      }
+      __syncthreads();
+    }
+    // compact table: replicas summed once, in parallel (packed tables already are compact)
+    const uint32_t comp_off = ((nw + 3u) & ~3u);
+    const bool compact = pack > 1 || (comp_off + 2u * C) * 4u <= dynamic_smem_bytes();
+    uint32_t* comp = pack > 1 ? s_marg : sh + comp_off;
+    if (compact && pack == 1) {
+      for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) comp[c] = rep_sum(c);
+      __syncthreads();
+    }
+    auto cell = [&](uint32_t c) -> uint32_t { return compact ? comp[c] : rep_sum(c); };
     if (q.nseg == 1) {
       if (tables) {
         uint32_t* t = tables + q.table_off;
         for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) t[c] = cell(c);
       }
-      if (want_score)
-        score_table(cell, C, q.r_target, m_total, flags, wi.q, ll_out, mi_out, nnz_out, ss);
+      if (want_score) {
+        if (compact)
+          score_cells(comp, C, q.r_target, pack > 1 ? s_nij : comp + C, m_total, flags, wi.q, ll_out,
+                      mi_out, nnz_out, ss);
+        else
+          score_table(cell, C, q.r_target, m_total, flags, wi.q, ll_out, mi_out, nnz_out, ss);
+      }
     } else {
       uint32_t* t = tables + q.table_off;
       for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
@@ -409,7 +634,7 @@ __global__ void __launch_bounds__(512, 2)
       reinterpret_cast<int4*>(&s_q)[threadIdx.x] =
           reinterpret_cast<const int4*>(qd + wi.q)[threadIdx.x];
     __syncthreads();
-    dispatch_rows<false>(s_q, wi.r0, wi.r1, nullptr, tables + s_q.table_off);
+    dispatch_global_rows(s_q, wi.r0, wi.r1, tables + s_q.table_off);
     __syncthreads();
   }
 }
@@ -537,6 +762,27 @@ __global__ void k_generate(uint8_t* __restrict__ col, int64_t m, uint64_t key, i
     int s = 0;
     for (int t = 0; t < rm1; ++t) s += (u >= __ldg(th + t)) ? 1 : 0;
     col[row] = (uint8_t)s;
+  }
+}
+
+// 4-bit copy of columns: output word w (rows 8w..8w+7) = row 8w+i in nibble i
+__global__ void k_pack4(const uint8_t* __restrict__ cols, int64_t ld, uint8_t* __restrict__ nib,
+                        int64_t ldn, int64_t m, int32_t var0, int32_t nvars) {
+  const int64_t words = (m + 7) >> 3;
+  for (int vv = blockIdx.y; vv < nvars; vv += gridDim.y) {
+    const uint8_t* c = cols + (int64_t)(var0 + vv) * ld;
+    uint32_t* o = reinterpret_cast<uint32_t*>(nib + (int64_t)(var0 + vv) * ldn);
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (int64_t)gridDim.x * blockDim.x) {
+      const uint2 b = *reinterpret_cast<const uint2*>(c + 8 * w);
+      // bytes x0..x3 of b.x -> nibbles 0..3, of b.y -> nibbles 4..7
+      uint32_t lo = b.x, hi = b.y;
+      lo = (lo | (lo >> 4)) & 0x00ff00ffu;   // [x0 | x1<<4, x2 | x3<<4] in 16-bit lanes
+      hi = (hi | (hi >> 4)) & 0x00ff00ffu;
+      lo = (lo | (lo >> 8)) & 0x0000ffffu;
+      hi = (hi | (hi >> 8)) & 0x0000ffffu;
+      o[w] = lo | (hi << 16);
+    }
   }
 }
 
