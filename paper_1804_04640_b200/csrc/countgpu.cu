@@ -78,7 +78,7 @@ using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, true> : nullptr},                           \
    {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, false> : nullptr,                           \
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, true> : nullptr},                           \
-   {k_hist<K, P_ROWS, false>, nullptr}}
+   {k_hist<K, P_ROWS, false>, k_hist<K, P_ROWS, true>}}
 static const HistFn kHist[CS_MAXK][4][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
 #undef CS_HK
@@ -179,6 +179,16 @@ struct cs_plan {
   uint32_t* d_tables = nullptr;  // plan-owned table buffer when the caller gives none
   size_t d_tables_cells = 0;
   const uint32_t* last_dtab = nullptr;  // device tables of the last execute
+  // chunked K2 work lists (built lazily): [0] = global-class queries, [1] = every query
+  struct ScoreList {
+    bool built = false;
+    int nlist = 0, nitems = 0;
+    char* blob = nullptr;  // [qlist | first | items | partials]
+    int32_t* qlist = nullptr;
+    int32_t* first = nullptr;
+    ScoreItem* items = nullptr;
+    double* part = nullptr;
+  } sl[2];
 };
 
 // ------------------------------------------------------------------------------------------
@@ -684,13 +694,13 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         }
         const int64_t left = smem_bytes - table_bytes(d);
         const int st = (int)std::min<int64_t>(4, left / std::max<int64_t>(per_stage, 1));
-        if (st >= 3 && (d.pack > 1 || d.mode == 0)) {
+        if (st >= 3 && (d.pack > 1 || d.mode <= 1)) {
           d.stages = st;
           d.stage_off = (uint32_t)table_bytes(d);
         }
       }
     }
-    if (d.kind == 0 && db->nib && (d.pack > 1 || d.mode == 0) && env_int("CS_NIBBLE", 1)) {
+    if (d.kind == 0 && db->nib && (d.pack > 1 || d.mode <= 1) && env_int("CS_NIBBLE", 1)) {
       d.nib = 1;
       d.base = db->nib;
       for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
@@ -770,8 +780,24 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     for (int i : groups[key]) sorted.push_back(items[i]);
   }
   p->nitems = (int)sorted.size();
-  for (size_t i = 0; i < order.size(); ++i)
-    if (p->hq[items[order[i]].q].kind == 1) sorted.push_back(items[order[i]]);
+  // global class: query-major (all segments of a query back to back, queries LPT by total
+  // cost) so concurrently running CTAs share one L2-resident table -- RED.ADD throughput
+  // collapses when they spray many >SMEM tables at once
+  {
+    std::map<int, double> qcost;
+    std::vector<int> gq;
+    for (size_t i = 0; i < items.size(); ++i)
+      if (p->hq[items[i].q].kind == 1) {
+        if (!qcost.count(items[i].q)) gq.push_back(items[i].q);
+        qcost[items[i].q] += cost[i];
+      }
+    std::stable_sort(gq.begin(), gq.end(), [&](int a, int b) { return qcost[a] > qcost[b]; });
+    std::map<int, std::vector<int>> byq;
+    for (size_t i = 0; i < items.size(); ++i)
+      if (p->hq[items[i].q].kind == 1) byq[items[i].q].push_back((int)i);
+    for (int qq : gq)
+      for (int i : byq[qq]) sorted.push_back(items[i]);
+  }
   p->ngitems = (int)sorted.size() - p->nitems;
   // upload descriptors (one blob through pinned staging)
   CS_CUDA(cudaSetDevice(ctx->device));
@@ -853,6 +879,11 @@ extern "C" int cs_plan_info(cs_plan* p, int64_t* cells, int64_t* table_off, int6
 extern "C" int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   cudaSetDevice(p->db->ctx->device);
+  for (auto& L : p->sl)
+    if (L.blob) {
+      cudaStreamSynchronize(p->db->ctx->stream);
+      cudaFree(L.blob);
+    }
   if (!p->transient) {
     cudaStreamSynchronize(p->db->ctx->stream);
     if (p->d_q) cudaFree((void*)p->d_q);  // blob base
@@ -946,6 +977,69 @@ static int finish_outputs(cs_ctx* ctx, OutBuf* obs, int nob) {
   return CS_OK;
 }
 
+// chunked K2 over a query list (which = 0: global-class score_list, 1: all queries)
+static int run_chunked_score(cs_plan* p, int which, const uint32_t* dtab, uint32_t flags, double* ll,
+                             double* mi, int64_t* nnz) {
+  cs_ctx* ctx = p->db->ctx;
+  auto& L = p->sl[which];
+  if (!L.built) {
+    std::vector<int32_t> qlist;
+    if (which == 0) qlist = p->score_list;
+    else {
+      qlist.resize(p->nq);
+      std::iota(qlist.begin(), qlist.end(), 0);
+    }
+    const uint32_t CH = 2048;  // configurations per CTA
+    std::vector<int32_t> first(1, 0);
+    std::vector<ScoreItem> items;
+    for (size_t i = 0; i < qlist.size(); ++i) {
+      const QDesc& d = p->hq[qlist[i]];
+      const uint32_t J = d.cells / (uint32_t)d.r_target;
+      for (uint32_t j0 = 0; j0 < J || (J == 0 && j0 == 0); j0 += CH) {
+        items.push_back(ScoreItem{qlist[i], (int32_t)i, j0, std::min(J, j0 + CH)});
+        if (J == 0) break;
+      }
+      first.push_back((int32_t)items.size());
+    }
+    const size_t b0 = sizeof(int32_t) * std::max<size_t>(qlist.size(), 1);
+    const size_t b1 = sizeof(int32_t) * first.size();
+    const size_t b2 = sizeof(ScoreItem) * std::max<size_t>(items.size(), 1);
+    const size_t b3 = sizeof(double) * 3 * std::max<size_t>(items.size(), 1);
+    const size_t o1 = round_up(b0, 256), o2 = o1 + round_up(b1, 256), o3 = o2 + round_up(b2, 256);
+    CS_CUDA(cudaMalloc(&L.blob, o3 + b3));
+    CS_CUDA(cudaMemcpy(L.blob, qlist.data(), sizeof(int32_t) * qlist.size(), cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(L.blob + o1, first.data(), b1, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(L.blob + o2, items.data(), sizeof(ScoreItem) * items.size(), cudaMemcpyHostToDevice));
+    L.qlist = (int32_t*)L.blob;
+    L.first = (int32_t*)(L.blob + o1);
+    L.items = (ScoreItem*)(L.blob + o2);
+    L.part = (double*)(L.blob + o3);
+    L.nlist = (int)qlist.size();
+    L.nitems = (int)items.size();
+    L.built = true;
+  }
+  if (L.nlist == 0) return CS_OK;
+  unsigned long long* qmarg = nullptr;
+  if (flags & F_MI) {
+    void* d = nullptr;
+    CS_TRY(ctx->scratch_get(19, sizeof(unsigned long long) * CS_MAX_ARITY * L.nlist, &d));
+    qmarg = (unsigned long long*)d;
+    CS_CUDA(cudaMemsetAsync(qmarg, 0, sizeof(unsigned long long) * CS_MAX_ARITY * L.nlist, ctx->stream));
+    k_score_marg<<<L.nitems, 256, 0, ctx->stream>>>(p->d_q, L.items, dtab, qmarg);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
+  const double m_total = (double)p->db->m_total;
+  k_score_part<<<L.nitems, 256, 0, ctx->stream>>>(p->d_q, L.items, dtab, qmarg, L.part, flags, m_total);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  k_score_reduce<<<(L.nlist + 255) / 256, 256, 0, ctx->stream>>>(L.qlist, L.first, L.nlist, L.part, ll, mi,
+                                                                  nnz, m_total);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
 extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, double* mi,
                                int64_t* nnz) {
   if (!p) return fail(CS_ERR_INVALID, "cs_plan_execute: NULL plan");
@@ -1003,12 +1097,8 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   }
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->ev_valid = true;
-  if (!partial && !p->score_list.empty() && (flags & (F_LOGLIK | F_MI | F_NNZ))) {
-    k_score<<<(unsigned)p->score_list.size(), 256, 0, ctx->stream>>>(
-        p->d_q, p->d_score_list, dtab, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev, flags, m_total);
-    ctx->launches++;
-    CS_CUDA(cudaGetLastError());
-  }
+  if (!partial && !p->score_list.empty() && (flags & (F_LOGLIK | F_MI | F_NNZ)))
+    CS_TRY(run_chunked_score(p, 0, dtab, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   OutBuf obs[4] = {tb, lb, mb, nb};
   return finish_outputs(ctx, obs, 4);
 }
@@ -1030,11 +1120,7 @@ extern "C" int cs_plan_score(cs_plan* p, const uint32_t* tables, double* loglik,
   CS_TRY(route(ctx, 2, loglik, sizeof(double) * p->nq, lb));
   CS_TRY(route(ctx, 3, mi, sizeof(double) * p->nq, mb));
   CS_TRY(route(ctx, 4, nnz, sizeof(int64_t) * p->nq, nb));
-  k_score<<<(unsigned)p->nq, 256, 0, ctx->stream>>>(p->d_q, nullptr, dtab, (double*)lb.dev,
-                                                     (double*)mb.dev, (int64_t*)nb.dev, flags,
-                                                     (double)p->db->m_total);
-  ctx->launches++;
-  CS_CUDA(cudaGetLastError());
+  CS_TRY(run_chunked_score(p, 1, dtab, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   OutBuf obs[3] = {lb, mb, nb};
   return finish_outputs(ctx, obs, 3);
 }

@@ -358,6 +358,63 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
 }
 
+// SMEM class, tables too large for 16-bit byte offsets (C*R*4 > 64 KB, C <= 65536): the
+// joint index is built in 16-bit lanes, and each row's counter address is one IMAD
+// (idx * 4R + 4 rep + base).
+template <int K, bool NIB>
+__device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int64_t r1,
+                                                 uint32_t* sh) {
+  constexpr int RPV = NIB ? 32 : 16;
+  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  uint32_t co[K], st[K];
+#pragma unroll
+  for (int v = 0; v < K; ++v) {
+    co[v] = q.coff[v];
+    st[v] = q.stride[v];
+  }
+  const int nbyte = q.nbyte;
+  const int rlog = q.rlog;
+  const uint32_t scale = 4u << rlog;
+  const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
+  char* rbase = reinterpret_cast<char*>(sh) + rep4;
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + RPV - 1) / RPV;
+  auto word = [&](const uint32_t (&w)[K]) {
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K; ++v)
+      if (v < nbyte) a8 += w[v] * st[v];
+    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K; ++v) {
+      if (v >= nbyte) {
+        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      }
+    }
+    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo & 0xffffu) * scale), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo >> 16) * scale), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi & 0xffffu) * scale), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi >> 16) * scale), 1u);
+  };
+  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+  if (q.stages >= 3) {
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
+  } else {
+    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+      uint32_t a[K][4];
+      load_vec16<K>(a, rowp + (vi << 4), co);
+      cnt(a);
+    }
+  }
+  const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
+    atomicSub(reinterpret_cast<uint32_t*>(rbase), (uint32_t)pad);
+}
+
 // SMEM class, tiny tables (C <= 41): PACK consecutive rows share one atomic.  The byte lanes
 // of a word hold 4 rows' joint indices (< C <= 255); one IDP4A per tuple folds them into the
 // tuple index  b0 + C b1 (+ C^2 b2 + C^3 b3)  of a C^PACK-cell table (32 replicas), so the
@@ -549,7 +606,7 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     if (PATH == P_LANE16) hist_smem_lane16<K, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
-    else hist_rows<K, 1, true>(q, wi.r0, wi.r1, sh, nullptr);
+    else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {
       uint32_t s = 0;
@@ -680,6 +737,92 @@ __global__ void k_family(int64_t nfam, const double* __restrict__ nlogn,
     const double v = nlogn[s_idx[f]] - (pi >= 0 ? nlogn[pi] : m_ln_m);
     if (ll) ll[f] = v;
     if (mdl) mdl[f] = -v + penalty[f];
+  }
+}
+
+// K2 (chunked): scores of global tables split into (query, config chunk) items so a 64 MB
+// table is read by many CTAs.  Pass "marg" (MI only) accumulates the target marginals N_k per
+// query; pass "part" writes one (LL, MI, nnz) partial per item; k_score_reduce sums a query's
+// partials in item order (deterministic).
+struct ScoreItem {
+  int32_t q;        // query (QDesc index)
+  int32_t li;       // position in the scored list (marginal slot)
+  uint32_t j0, j1;  // configuration range [j0, j1)
+};
+
+__global__ void k_score_marg(const QDesc* __restrict__ qd, const ScoreItem* __restrict__ items,
+                             const uint32_t* __restrict__ tables, unsigned long long* qmarg) {
+  __shared__ unsigned long long sm[CS_MAX_ARITY];
+  const ScoreItem it = items[blockIdx.x];
+  const QDesc& d = qd[it.q];
+  const int rt = d.r_target;
+  for (int k = threadIdx.x; k < rt; k += blockDim.x) sm[k] = 0ull;
+  __syncthreads();
+  const uint32_t* t = tables + d.table_off;
+  for (uint64_t c = (uint64_t)it.j0 * rt + threadIdx.x; c < (uint64_t)it.j1 * rt; c += blockDim.x) {
+    const uint32_t v = t[c];
+    if (v) atomicAdd(&sm[c % (uint64_t)rt], (unsigned long long)v);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < rt; k += blockDim.x)
+    if (sm[k]) atomicAdd(qmarg + (int64_t)it.li * CS_MAX_ARITY + k, sm[k]);
+}
+
+__global__ void k_score_part(const QDesc* __restrict__ qd, const ScoreItem* __restrict__ items,
+                             const uint32_t* __restrict__ tables,
+                             const unsigned long long* __restrict__ qmarg, double* part,
+                             uint32_t flags, double m_total) {
+  __shared__ double red[32];
+  __shared__ unsigned long long redu[32];
+  const ScoreItem it = items[blockIdx.x];
+  const QDesc& d = qd[it.q];
+  const int rt = d.r_target;
+  const uint32_t* t = tables + d.table_off;
+  const bool want_mi = (flags & F_MI) != 0;
+  const bool nlogn = (flags & F_NLOGN) != 0;
+  const unsigned long long* mg = qmarg + (int64_t)it.li * CS_MAX_ARITY;
+  double ll = 0.0, mi = 0.0;
+  unsigned long long nz = 0;
+  for (uint32_t j = it.j0 + threadIdx.x; j < it.j1; j += blockDim.x) {
+    const uint32_t* row = t + (uint64_t)j * rt;
+    unsigned long long nij = 0;
+    for (int k = 0; k < rt; ++k) nij += row[k];
+    if (!nij) continue;
+    const double dnij = (double)nij;
+    for (int k = 0; k < rt; ++k) {
+      const uint32_t n = row[k];
+      if (!n) continue;
+      const double x = (double)n;
+      ++nz;
+      ll += nlogn ? x * log(x) : x * log(x / dnij);
+      if (want_mi) mi += x * log((x * m_total) / (dnij * (double)mg[k]));
+    }
+  }
+  const double tll = block_sum(ll, red);
+  const double tmi = want_mi ? block_sum(mi, red) : 0.0;
+  const unsigned long long tnz = block_sum_u64(nz, redu);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = tll;
+    part[3 * blockIdx.x + 1] = tmi;
+    part[3 * blockIdx.x + 2] = (double)tnz;
+  }
+}
+
+// one thread per listed query: sum its items' partials in order
+__global__ void k_score_reduce(const int32_t* __restrict__ qlist, const int32_t* __restrict__ first,
+                               int nlist, const double* __restrict__ part, double* ll_out,
+                               double* mi_out, int64_t* nnz_out, double m_total) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nlist; i += gridDim.x * blockDim.x) {
+    double ll = 0.0, mi = 0.0, nz = 0.0;
+    for (int it = first[i]; it < first[i + 1]; ++it) {
+      ll += part[3 * it];
+      mi += part[3 * it + 1];
+      nz += part[3 * it + 2];
+    }
+    const int q = qlist[i];
+    if (ll_out) ll_out[q] = ll;
+    if (mi_out) mi_out[q] = mi / m_total;
+    if (nnz_out) nnz_out[q] = (int64_t)nz;
   }
 }
 

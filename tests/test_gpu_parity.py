@@ -322,3 +322,53 @@ def test_duck_typed_reference_objects(reference_cases):
     col = cs.RecordCollector()
     s.query(RefQuery(1, (2, 0)), col)
     assert _recs(col.result()) == FIXTURE_X1_GIVEN_X0_X2
+
+
+@pytest.mark.parametrize("smem_kb", ["220", "8"])
+def test_instance_sharded_merge_on_one_gpu(smem_kb):
+    """CS_PARTIAL tables of two row shards, summed on the device, then cs_plan_score with the
+    global m (the cfg5 NCCL path minus the collective) == oracle LL / MI on the full data.
+    smem_kb=8 forces the global-atomic class and the chunked K2 scorer."""
+    import torch
+
+    old = os.environ.get("CS_HIST_SMEM_KB")
+    os.environ["CS_HIST_SMEM_KB"] = smem_kb
+    try:
+        c = cs.GpuContext(0)
+        w = workloads.cfg5(nq=40, m=300_001, n=30, seed=7)
+        cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+        u8 = np.vstack([cols[v] for v in range(w.n)])
+        from paper_1804_04640_b200.parallel import shard_rows
+
+        parts = []
+        for r in range(2):
+            r0, nr = shard_rows(w.m, 2, r)
+            g = w.build_device(c, row_offset=r0, m_shard=nr)
+            assert np.array_equal(g.download(3), u8[3, r0:r0 + nr])
+            plan = QueryPlan(g, w.queries, cs._native.CS_PARTIAL | cs._native.CS_WANT_TABLES)
+            t = torch.zeros(plan.total_cells, dtype=torch.int32, device="cuda")
+            plan.execute(tables=t)
+            parts.append((g, plan, t))
+        c.sync()  # device outputs are asynchronous on the context stream
+        merged = parts[0][2] + parts[1][2]
+        torch.cuda.synchronize()
+        plan = parts[1][1]
+        ll = torch.zeros(plan.nq, dtype=torch.float64, device="cuda")
+        mi = torch.zeros(plan.nq, dtype=torch.float64, device="cuda")
+        nnz = torch.zeros(plan.nq, dtype=torch.int64, device="cuda")
+        plan.score(merged, loglik=ll, mi=mi, nnz=nnz)
+        c.sync()
+        otabs, _, oll, onnz = O.radix_tables(u8, w.arities, w.queries)
+        assert np.array_equal(merged.cpu().numpy().view(np.uint32), otabs)
+        assert np.allclose(ll.cpu().numpy(), oll, rtol=1e-9, atol=1e-9)
+        assert np.array_equal(nnz.cpu().numpy(), onnz)
+        for i, q in enumerate(w.queries[:25]):
+            recs = O.oracle_records(u8, w.arities, q[0], q[1:])
+            ll0 = O.loglik_of_records(O.oracle_records(u8, w.arities, q[0], ()))
+            tol = 1e-9 * (abs(oll[i]) + abs(ll0)) / w.m
+            assert abs(mi[i].item() - O.mi_of_records(recs, w.m)) <= tol
+    finally:
+        if old is None:
+            os.environ.pop("CS_HIST_SMEM_KB", None)
+        else:
+            os.environ["CS_HIST_SMEM_KB"] = old
