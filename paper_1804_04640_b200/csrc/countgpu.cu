@@ -78,13 +78,17 @@ using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, true> : nullptr},                           \
    {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, false> : nullptr,                           \
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, true> : nullptr},                           \
-   {k_hist<K, P_ROWS, false>, k_hist<K, P_ROWS, true>}}
-static const HistFn kHist[CS_MAXK][4][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
+   {k_hist<K, P_ROWS, false>, k_hist<K, P_ROWS, true>},                                   \
+   {k_hist<K, P_HALF, false>, k_hist<K, P_HALF, true>}}
+static const HistFn kHist[CS_MAXK][5][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
 #undef CS_HK
 
 static int hist_path(const QDesc& d) {
-  return d.pack == 4 ? P_PACK4 : (d.pack == 2 ? P_PACK2 : (d.mode == 0 ? P_LANE16 : P_ROWS));
+  if (d.pack == 4) return P_PACK4;
+  if (d.pack == 2) return P_PACK2;
+  if (d.half) return P_HALF;
+  return d.mode == 0 ? P_LANE16 : P_ROWS;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -667,6 +671,17 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       while (rl < 5 && (c << (rl + 1)) <= smem_words) ++rl;
       d.rlog = rl;
       d.mode = (c << rl) <= 16384 ? 0 : (c <= 65536 ? 1 : 2);
+      // 16-bit counters (two cells per word) double the replicas when 32-bit ones are short of
+      // 32; counters cannot overflow while every replica serves <= 65535 rows of an item
+      const int64_t seg_cap = std::min<int64_t>(m, (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22));
+      if (d.rlog < 5 && c <= 65536 && env_int("CS_HALF", 0)) {  // measured slower on cfg2: opt-in
+        int rh = 0;
+        while (rh < 5 && (((c + 1) / 2) << (rh + 1)) <= smem_words) ++rh;
+        if (rh > d.rlog && seg_cap <= (65535LL << rh)) {
+          d.half = 1;
+          d.rlog = rh;
+        }
+      }
     } else {
       d.kind = 1;
       d.mode = c <= 65536 ? 1 : 2;
@@ -679,6 +694,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       auto table_bytes = [&](const QDesc& x) {
         int64_t ct = x.cells;
         for (int i = 1; i < x.pack; ++i) ct *= x.cells;
+        if (x.half) ct = (ct + 1) / 2;
         return round_up((ct << x.rlog) * 4, 128);
       };
       if (k <= 4 && env_int("CS_STAGES", 1)) {
@@ -761,12 +777,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   });
   // SMEM-class items grouped by K1 variant (k, path, layout), groups by descending total cost,
   // LPT order inside a group; then the global-class items.
-  std::map<int, std::vector<int>> groups;  // key = (k-1)*8 + path*2 + nib
+  std::map<int, std::vector<int>> groups;  // key = (k-1)*16 + path*2 + nib
   std::map<int, double> gcost;
   for (size_t i = 0; i < order.size(); ++i) {
     const QDesc& d = p->hq[items[order[i]].q];
     if (d.kind != 0) continue;
-    const int key = (d.k - 1) * 8 + hist_path(d) * 2 + d.nib;
+    const int key = (d.k - 1) * 16 + hist_path(d) * 2 + d.nib;
     groups[key].push_back(order[i]);
     gcost[key] += cost[order[i]];
   }
@@ -1077,7 +1093,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   if (p->nitems > 0) {
     for (size_t g = 0; g < p->groups.size(); ++g) {
       const auto& G = p->groups[g];
-      const int k = G.key / 8 + 1, path = (G.key % 8) / 2, nib = G.key % 2;
+      const int k = G.key / 16 + 1, path = (G.key % 16) / 2, nib = G.key % 2;
       HistFn f = kHist[k - 1][path][nib];
       if (!f) return fail(CS_ERR_INVALID, "internal: no K1 variant for k=%d path=%d", k, path);
       const int grid = std::min(ctx->hist_ctas, G.count);

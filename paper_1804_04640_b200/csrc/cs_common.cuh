@@ -39,6 +39,7 @@ struct __align__(16) QDesc {
   int32_t stages;               // SMEM class: cp.async prefetch ring depth (0 = direct loads)
   uint32_t stage_off;           // SMEM class: byte offset of the ring in dynamic SMEM
   int32_t nib;                  // 1: columns read from the 4-bit (nibble) copy, 32 rows / 16 B
+  int32_t half;                 // 1: 16-bit counters, two cells per word (hist_smem_half)
 };
 
 // One unit of work: rows [r0, r1) of query q.

@@ -358,6 +358,67 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
 }
 
+// SMEM class, 16-bit counters (two cells per 32-bit word: cell c lives in word c >> 1, half
+// c & 1, of its replica), which doubles the replica count R that fits -- R = 32 (lane-private,
+// bank-conflict-free) up to 3520 cells instead of 1760.  The host enables it only when a
+// counter cannot overflow: rows per item <= 65535 * R (each replica serves rows / R rows).
+template <int K, bool NIB>
+__device__ __forceinline__ void hist_smem_half(const QDesc& q, int64_t r0, int64_t r1,
+                                               uint32_t* sh) {
+  constexpr int RPV = NIB ? 32 : 16;
+  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  uint32_t co[K], st[K];
+#pragma unroll
+  for (int v = 0; v < K; ++v) {
+    co[v] = q.coff[v];
+    st[v] = q.stride[v];
+  }
+  const int nbyte = q.nbyte;
+  const int rlog = q.rlog;
+  const uint32_t scale2 = 2u << rlog;  // bytes per cell pair per replica / 2
+  const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
+  char* rbase = reinterpret_cast<char*>(sh) + rep4;
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + RPV - 1) / RPV;
+  auto bump = [&](uint32_t c) {
+    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (c & ~1u) * scale2), 1u << ((c & 1u) << 4));
+  };
+  auto word = [&](const uint32_t (&w)[K]) {
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K; ++v)
+      if (v < nbyte) a8 += w[v] * st[v];
+    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K; ++v) {
+      if (v >= nbyte) {
+        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      }
+    }
+    bump(lo & 0xffffu);
+    bump(lo >> 16);
+    bump(hi & 0xffffu);
+    bump(hi >> 16);
+  };
+  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+  if (q.stages >= 3) {
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
+  } else {
+    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+      uint32_t a[K][4];
+      load_vec16<K>(a, rowp + (vi << 4), co);
+      cnt(a);
+    }
+  }
+  const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0 (low half)
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
+    atomicSub(reinterpret_cast<uint32_t*>(rbase), (uint32_t)pad);
+}
+
 // SMEM class, tables too large for 16-bit byte offsets (C*R*4 > 64 KB, C <= 65536): the
 // joint index is built in 16-bit lanes, and each row's counter address is one IMAD
 // (idx * 4R + 4 rep + base).
@@ -567,7 +628,7 @@ __device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0,
 // An SMEM item finishes with the fused epilogue: a single-segment query writes its table and
 // scores straight from SMEM; a multi-segment query adds its partial table into global memory
 // and the last segment to arrive (done counter) scores the merged table.
-enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3 };
+enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4 };
 constexpr int CS_HIST_THREADS = 1024;
 
 template <int K, int PATH, bool NIB>
@@ -599,18 +660,24 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     const uint32_t C = q.cells;
     uint32_t ct = C;  // cells of the SMEM table (C^pack for packed tuples)
     for (int i = 1; i < pack; ++i) ct *= C;
-    const uint32_t nw = ct << rl;
+    const uint32_t nw = (PATH == P_HALF ? (C + 1u) >> 1 : ct) << rl;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
     if (threadIdx.x < 64) s_marg[threadIdx.x] = 0u;
     __syncthreads();
     if (PATH == P_LANE16) hist_smem_lane16<K, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
+    else if (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
     else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {
       uint32_t s = 0;
-      for (uint32_t r = 0; r < R; ++r) s += sh[(c << rl) | ((r + c) & (R - 1u))];
+      if (PATH == P_HALF) {
+        const uint32_t p = c >> 1, sh16 = (c & 1u) << 4;
+        for (uint32_t r = 0; r < R; ++r) s += (sh[(p << rl) | ((r + p) & (R - 1u))] >> sh16) & 0xffffu;
+      } else {
+        for (uint32_t r = 0; r < R; ++r) s += sh[(c << rl) | ((r + c) & (R - 1u))];
+      }
       return s;
     };
     if (pack > 1) {
