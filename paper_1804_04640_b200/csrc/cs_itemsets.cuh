@@ -21,7 +21,7 @@ namespace cs {
 constexpr int IS_ROWS = 128;   // rows per tile (32 lanes x 4)
 constexpr int IS_COLS = 32;    // columns per tile (8 warps x 4)
 constexpr int IS_TW = 32;      // words per k-step
-constexpr int IS_XS = IS_TW + 1;  // padded smem row stride (conflict-free lane-per-row reads)
+constexpr int IS_XS = IS_TW + 2;  // padded smem row stride: lane-per-row LDS.64 conflict-free
 constexpr int IS_THREADS = 256;
 
 struct ISRow {
@@ -50,8 +50,8 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
     k_itemsets(const uint32_t* const* __restrict__ plane, const ISRow* __restrict__ rows, int nrows,
                int n, const ISUnit* __restrict__ units, int nunits, int* __restrict__ head,
                unsigned long long* pairs, unsigned long long* triples) {
-  __shared__ uint32_t xs[IS_ROWS * IS_XS];
-  __shared__ uint32_t ys[IS_COLS * IS_TW];
+  __shared__ __align__(16) uint32_t xs[IS_ROWS * IS_XS];
+  __shared__ __align__(16) uint32_t ys[IS_COLS * IS_TW];
   __shared__ int s_unit;
   __shared__ ISRow s_rows[IS_ROWS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
           const uint4 pb = *reinterpret_cast<const uint4*>(plane[rr.b] + w0 + 4 * q);
           x = make_uint4(pa.x & pb.x, pa.y & pb.y, pa.z & pb.z, pa.w & pb.w);
         }
-        uint32_t* d = xs + r * IS_XS + 4 * q;
-        d[0] = x.x; d[1] = x.y; d[2] = x.z; d[3] = x.w;
+        uint2* d = reinterpret_cast<uint2*>(xs + r * IS_XS + 4 * q);
+        d[0] = make_uint2(x.x, x.y);
+        d[1] = make_uint2(x.z, x.w);
       }
       for (int e = threadIdx.x; e < IS_COLS * (IS_TW / 4); e += IS_THREADS) {
         const int c = e / (IS_TW / 4), q = e % (IS_TW / 4);
@@ -102,13 +103,15 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
           uint32_t x0[4], x1[4], y0[4], y1[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            x0[i] = xs[(lane + 32 * i) * IS_XS + k];
-            x1[i] = xs[(lane + 32 * i) * IS_XS + k + 1];
+            const uint2 t = *reinterpret_cast<const uint2*>(xs + (lane + 32 * i) * IS_XS + k);
+            x0[i] = t.x;
+            x1[i] = t.y;
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            y0[j] = ys[(warp * 4 + j) * IS_TW + k];
-            y1[j] = ys[(warp * 4 + j) * IS_TW + k + 1];
+            const uint2 t = *reinterpret_cast<const uint2*>(ys + (warp * 4 + j) * IS_TW + k);
+            y0[j] = t.x;
+            y1[j] = t.y;
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -120,13 +123,15 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
           uint32_t x2[4], x3[4], y2[4], y3[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            x2[i] = xs[(lane + 32 * i) * IS_XS + k + 2];
-            x3[i] = xs[(lane + 32 * i) * IS_XS + k + 3];
+            const uint2 t = *reinterpret_cast<const uint2*>(xs + (lane + 32 * i) * IS_XS + k + 2);
+            x2[i] = t.x;
+            x3[i] = t.y;
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            y2[j] = ys[(warp * 4 + j) * IS_TW + k + 2];
-            y3[j] = ys[(warp * 4 + j) * IS_TW + k + 3];
+            const uint2 t = *reinterpret_cast<const uint2*>(ys + (warp * 4 + j) * IS_TW + k + 2);
+            y2[j] = t.x;
+            y3[j] = t.y;
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
