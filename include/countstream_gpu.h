@@ -115,7 +115,11 @@ int cs_bitmap_plane(cs_db* db, int32_t var, int32_t state, const uint32_t** dev,
 /* ---- counting queries (reference radix.py:113-156, bitmap.py:69-128) ----------------- */
 /* Query q uses vars[var_off[q] .. var_off[q+1]): target first, then parents in the
  * reference's given order (QuerySpec(target, parents), database.py:102-126).
- * Cells are packed: table of q starts at table_off[q] = sum_{p<q} cells[p]. */
+ * Cells are packed: table of q starts at table_off[q] = sum_{p<q} cells[p].
+ * Joint state spaces above the dense limit (2^30 cells; env CS_MAX_DENSE_LOG2) are counted in
+ * device hash tables instead (any number of variables, up to 2^63 cells): such a query has
+ * cells[q] = 0 in the dense layout; its LL / MI / nnz outputs and its cs_plan_compact record
+ * stream (hash order) are produced as for dense queries.  Not combinable with CS_PARTIAL. */
 int cs_plan_create(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                    uint32_t flags, cs_plan** out);
 /* cells: host int64[nq] (nullable); table_off: host int64[nq] (nullable); total cells */

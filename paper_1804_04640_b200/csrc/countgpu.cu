@@ -165,6 +165,19 @@ struct cs_plan {
   bool needs_zero = false;     // tables must be zeroed before K1
   bool transient = false;      // one-shot plan (cs_query_batch): buffers come from ctx scratch
   std::vector<int32_t> score_list;    // queries scored by K2 after K1 (kind 1/2)
+  struct SparseQ {  // kind 3: hash-counted queries (no dense table)
+    int32_t q = 0, k = 0, rt = 0;
+    uint64_t C = 0, H = 0;
+    std::vector<int32_t> vars;
+    std::vector<unsigned long long> stride;
+    char* blob = nullptr;  // [vars | stride | keys | pkeys | cnt | pcnt | part]
+    int32_t* d_vars = nullptr;
+    unsigned long long *d_stride = nullptr, *keys = nullptr, *pkeys = nullptr;
+    uint32_t *cnt = nullptr, *pcnt = nullptr;
+    double* part = nullptr;
+    int nparts = 0;
+  };
+  std::vector<SparseQ> sparse;
   std::vector<int32_t> generic_list;  // kind 2 queries
   struct Group {
     int key, first, count;
@@ -636,23 +649,44 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         d.coff[i] = (uint32_t)((int64_t)v * (db->ld / 256));
         d.stride[i] = (uint32_t)c;
       }
-      c *= db->arity[v];
-      if (c > ((int64_t)1 << max_dense)) {
+      if (c > (int64_t)(((uint64_t)1 << 63) - 1) / db->arity[v]) {
         delete p;
-        return fail(CS_ERR_UNSUPPORTED,
-                    "query %d: joint state space exceeds the dense-table limit 2^%lld cells", q,
-                    (long long)max_dense);
+        return fail(CS_ERR_UNSUPPORTED, "query %d: joint state space exceeds 2^63 cells", q);
       }
+      c *= db->arity[v];
       if (c <= 256) nbyte = i + 1;
     }
     d.base = db->cols;
+    const bool sparse = c > ((int64_t)1 << max_dense);
+    if (sparse && (flags & F_PARTIAL)) {
+      delete p;
+      return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", q);
+    }
     d.k = k;
-    d.cells = (uint32_t)c;
+    d.cells = sparse ? 0u : (uint32_t)c;
     d.nbyte = std::max(nbyte, 1);
     d.mode = c <= 65536 ? 1 : 2;
     d.r_target = db->arity[vars[b]];
     d.table_off = total;
-    if (k > CS_MAXK) {
+    if (sparse) {
+      d.kind = 3;
+      cs_plan::SparseQ sq;
+      sq.q = q;
+      sq.k = k;
+      sq.rt = db->arity[vars[b]];
+      sq.C = (uint64_t)c;
+      uint64_t st = 1;
+      for (int i = 0; i < k; ++i) {
+        sq.vars.push_back(vars[b + i]);
+        sq.stride.push_back(st);
+        st *= (uint64_t)db->arity[vars[b + i]];
+      }
+      uint64_t H = 1024;
+      while (H < 2 * std::min<uint64_t>((uint64_t)m, sq.C)) H <<= 1;
+      sq.H = H;
+      p->sparse.push_back(sq);
+      c = 0;  // no dense table
+    } else if (k > CS_MAXK) {
       d.kind = 2;
       d.var_base = (int32_t)gvars.size();
       int64_t s = 1;
@@ -741,6 +775,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   std::vector<double> cost;
   for (int q = 0; q < nq; ++q) {
     QDesc& d = p->hq[q];
+    if (d.kind == 3) {
+      d.nseg = 1;
+      continue;
+    }
     if (d.kind == 2) {
       p->generic_list.push_back(q);
       p->score_list.push_back(q);
@@ -902,6 +940,11 @@ extern "C" int cs_plan_info(cs_plan* p, int64_t* cells, int64_t* table_off, int6
 extern "C" int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   cudaSetDevice(p->db->ctx->device);
+  for (auto& sq : p->sparse)
+    if (sq.blob) {
+      cudaStreamSynchronize(p->db->ctx->stream);
+      cudaFree(sq.blob);
+    }
   for (auto& L : p->sl)
     if (L.blob) {
       cudaStreamSynchronize(p->db->ctx->stream);
@@ -997,6 +1040,66 @@ static int finish_outputs(cs_ctx* ctx, OutBuf* obs, int nob) {
     }
   }
   if (any_host) CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+// sparse (hash) query: count into the two hash tables, then score from them
+static int run_sparse(cs_plan* p, cs_plan::SparseQ& sq, uint32_t flags, double* ll, double* mi,
+                      int64_t* nnz) {
+  cs_db* db = p->db;
+  cs_ctx* ctx = db->ctx;
+  const int nparts = (int)std::min<uint64_t>((sq.H + 255) / 256, (uint64_t)ctx->num_sms * 8);
+  if (!sq.blob) {
+    const size_t bv = round_up(sizeof(int32_t) * sq.k, 256), bs = round_up(sizeof(uint64_t) * sq.k, 256);
+    const size_t bk = round_up(8 * sq.H, 256), bc = round_up(4 * sq.H, 256), bp = round_up(24 * nparts, 256);
+    cudaError_t e = cudaMalloc(&sq.blob, bv + bs + 2 * bk + 2 * bc + bp);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      sq.blob = nullptr;
+      return fail(CS_ERR_OOM, "sparse query %d: cannot allocate hash tables of %llu slots", sq.q,
+                  (unsigned long long)sq.H);
+    }
+    char* o = sq.blob;
+    sq.d_vars = (int32_t*)o;
+    o += bv;
+    sq.d_stride = (unsigned long long*)o;
+    o += bs;
+    sq.keys = (unsigned long long*)o;
+    o += bk;
+    sq.pkeys = (unsigned long long*)o;
+    o += bk;
+    sq.cnt = (uint32_t*)o;
+    o += bc;
+    sq.pcnt = (uint32_t*)o;
+    o += bc;
+    sq.part = (double*)o;
+    sq.nparts = nparts;
+    CS_CUDA(cudaMemcpy(sq.d_vars, sq.vars.data(), sizeof(int32_t) * sq.k, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(sq.d_stride, sq.stride.data(), sizeof(uint64_t) * sq.k, cudaMemcpyHostToDevice));
+  }
+  CS_CUDA(cudaMemsetAsync(sq.keys, 0xff, 2 * round_up(8 * sq.H, 256), ctx->stream));
+  CS_CUDA(cudaMemsetAsync(sq.cnt, 0, 2 * round_up(4 * sq.H, 256), ctx->stream));
+  const unsigned grid = (unsigned)std::min<int64_t>((db->m + 255) / 256, (int64_t)ctx->num_sms * 8);
+  k_sparse_count<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, db->m, sq.d_vars, sq.d_stride, sq.k, sq.rt,
+                                                sq.keys, sq.cnt, sq.pkeys, sq.pcnt, sq.H - 1);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  if ((flags & F_PARTIAL) || !(flags & (F_LOGLIK | F_MI | F_NNZ))) return CS_OK;
+  unsigned long long* qmarg = nullptr;
+  if (flags & F_MI) {
+    void* d = nullptr;
+    CS_TRY(ctx->scratch_get(20, sizeof(unsigned long long) * CS_MAX_ARITY, &d));
+    qmarg = (unsigned long long*)d;
+    CS_CUDA(cudaMemsetAsync(qmarg, 0, sizeof(unsigned long long) * CS_MAX_ARITY, ctx->stream));
+    k_sparse_marg<<<sq.nparts, 256, 0, ctx->stream>>>(sq.keys, sq.cnt, sq.H, sq.rt, qmarg);
+    ctx->launches++;
+  }
+  const double m_total = (double)db->m_total;
+  k_sparse_part<<<sq.nparts, 256, 0, ctx->stream>>>(sq.keys, sq.cnt, sq.pkeys, sq.pcnt, sq.H, sq.rt, qmarg,
+                                                    flags, m_total, sq.part);
+  k_sparse_reduce<<<1, 32, 0, ctx->stream>>>(sq.part, sq.nparts, sq.q, ll, mi, nnz, m_total);
+  ctx->launches += 2;
+  CS_CUDA(cudaGetLastError());
   return CS_OK;
 }
 
@@ -1118,6 +1221,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
   }
+  for (auto& sq : p->sparse) CS_TRY(run_sparse(p, sq, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->ev_valid = true;
   if (!partial && !p->score_list.empty() && (flags & (F_LOGLIK | F_MI | F_NNZ)))
@@ -1168,6 +1272,20 @@ extern "C" int cs_plan_compact(cs_plan* p, const uint32_t* tables, const int64_t
                                                        (int64_t*)a.dev, (int64_t*)b.dev, (int64_t*)c.dev);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
+  if (!p->sparse.empty()) {
+    void* dpos = nullptr;
+    CS_TRY(ctx->scratch_get(21, sizeof(unsigned long long) * p->sparse.size(), &dpos));
+    CS_CUDA(cudaMemsetAsync(dpos, 0, sizeof(unsigned long long) * p->sparse.size(), ctx->stream));
+    for (size_t i = 0; i < p->sparse.size(); ++i) {
+      auto& sq = p->sparse[i];
+      if (!sq.blob) return fail(CS_ERR_INVALID, "cs_plan_compact: execute the plan first");
+      k_sparse_compact<<<(unsigned)std::max(sq.nparts, 1), 256, 0, ctx->stream>>>(
+          sq.keys, sq.cnt, sq.pkeys, sq.pcnt, sq.H, sq.rt, out_off[sq.q], (unsigned long long*)dpos + i,
+          (int64_t*)a.dev, (int64_t*)b.dev, (int64_t*)c.dev);
+      ctx->launches++;
+      CS_CUDA(cudaGetLastError());
+    }
+  }
   OutBuf obs[3] = {a, b, c};
   CS_TRY(finish_outputs(ctx, obs, 3));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));  // out_off staging reused next call

@@ -893,6 +893,127 @@ __global__ void k_score_reduce(const int32_t* __restrict__ qlist, const int32_t*
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Sparse class: joint state spaces too large for a dense table (any number of variables, up to
+// 2^63 cells).  Each row's 64-bit joint index (same convention) and its parent-configuration
+// index (index / r_t) are counted in two open-addressing hash tables (linear probing, CAS
+// insert); the scores and the record stream are read back from the hash.  The reference's
+// radix strategy handles such queries by partitioning (radix.py:113-156) -- this is the GPU
+// equivalent of its hash baseline's keys (baselines.py:38-74).
+constexpr unsigned long long CS_EMPTY_KEY = ~0ull;
+
+__device__ __forceinline__ void hash_count(unsigned long long* keys, uint32_t* cnt, uint64_t mask,
+                                           unsigned long long key) {
+  uint64_t slot = mix64(key) & mask;
+  for (;;) {
+    const unsigned long long prev = atomicCAS(keys + slot, CS_EMPTY_KEY, key);
+    if (prev == CS_EMPTY_KEY || prev == key) {
+      atomicAdd(cnt + slot, 1u);
+      return;
+    }
+    slot = (slot + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ uint32_t hash_lookup(const unsigned long long* keys, const uint32_t* cnt,
+                                                uint64_t mask, unsigned long long key) {
+  uint64_t slot = mix64(key) & mask;
+  for (;;) {
+    const unsigned long long k = keys[slot];
+    if (k == key) return cnt[slot];
+    if (k == CS_EMPTY_KEY) return 0u;
+    slot = (slot + 1) & mask;
+  }
+}
+
+__global__ void k_sparse_count(const uint8_t* __restrict__ cols, int64_t ld, int64_t m,
+                               const int32_t* __restrict__ vars, const unsigned long long* __restrict__ stride,
+                               int k, int rt, unsigned long long* keys, uint32_t* cnt,
+                               unsigned long long* pkeys, uint32_t* pcnt, uint64_t mask) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0, pkey = 0;
+    for (int v = 0; v < k; ++v) {
+      const unsigned long long s = __ldg(cols + (int64_t)vars[v] * ld + row);
+      key += s * stride[v];
+      if (v > 0) pkey += s * (stride[v] / (unsigned long long)rt);
+    }
+    hash_count(keys, cnt, mask, key);
+    hash_count(pkeys, pcnt, mask, pkey);
+  }
+}
+
+__global__ void k_sparse_marg(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ cnt,
+                              uint64_t H, int rt, unsigned long long* qmarg) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (cnt[i]) atomicAdd(qmarg + keys[i] % (unsigned long long)rt, (unsigned long long)cnt[i]);
+}
+
+__global__ void k_sparse_part(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ cnt,
+                              const unsigned long long* __restrict__ pkeys, const uint32_t* __restrict__ pcnt,
+                              uint64_t H, int rt, const unsigned long long* __restrict__ qmarg,
+                              uint32_t flags, double m_total, double* part) {
+  __shared__ double red[32];
+  __shared__ unsigned long long redu[32];
+  const bool want_mi = (flags & F_MI) != 0, nlogn = (flags & F_NLOGN) != 0;
+  double ll = 0.0, mi = 0.0;
+  unsigned long long nz = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = cnt[i];
+    if (!n) continue;
+    const double x = (double)n;
+    ++nz;
+    if (nlogn) {
+      ll += x * log(x);
+      continue;
+    }
+    const unsigned long long key = keys[i];
+    const double dnij = (double)hash_lookup(pkeys, pcnt, H - 1, key / (unsigned long long)rt);
+    ll += x * log(x / dnij);
+    if (want_mi) mi += x * log((x * m_total) / (dnij * (double)qmarg[key % (unsigned long long)rt]));
+  }
+  const double tll = block_sum(ll, red);
+  const double tmi = want_mi ? block_sum(mi, red) : 0.0;
+  const unsigned long long tnz = block_sum_u64(nz, redu);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = tll;
+    part[3 * blockIdx.x + 1] = tmi;
+    part[3 * blockIdx.x + 2] = (double)tnz;
+  }
+}
+
+__global__ void k_sparse_reduce(const double* __restrict__ part, int nparts, int q, double* ll_out,
+                                double* mi_out, int64_t* nnz_out, double m_total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double ll = 0.0, mi = 0.0, nz = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    ll += part[3 * i];
+    mi += part[3 * i + 1];
+    nz += part[3 * i + 2];
+  }
+  if (ll_out) ll_out[q] = ll;
+  if (mi_out) mi_out[q] = mi / m_total;
+  if (nnz_out) nnz_out[q] = (int64_t)nz;
+}
+
+__global__ void k_sparse_compact(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ cnt,
+                                 const unsigned long long* __restrict__ pkeys,
+                                 const uint32_t* __restrict__ pcnt, uint64_t H, int rt, int64_t base,
+                                 unsigned long long* pos, int64_t* cidx, int64_t* nijk, int64_t* nij) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = cnt[i];
+    if (!n) continue;
+    const unsigned long long key = keys[i];
+    const int64_t o = base + (int64_t)atomicAdd(pos, 1ull);
+    cidx[o] = (int64_t)key;
+    nijk[o] = n;
+    nij[o] = hash_lookup(pkeys, pcnt, H - 1, key / (unsigned long long)rt);
+  }
+}
+
 // K5: non-zero cells of each table in ascending cell order.  One CTA per query.
 __global__ void k_compact(const QDesc* __restrict__ qd, const uint32_t* __restrict__ tables,
                           const int64_t* __restrict__ out_off, int64_t* cidx, int64_t* nijk,

@@ -372,3 +372,45 @@ def test_instance_sharded_merge_on_one_gpu(smem_kb):
             os.environ.pop("CS_HIST_SMEM_KB", None)
         else:
             os.environ["CS_HIST_SMEM_KB"] = old
+
+
+def test_sparse_hash_class(random_sweep):
+    """Joint state spaces beyond the dense limit go to the hash class: forced with a tiny dense
+    limit on the random sweep, plus a genuine 2^40-cell query (40 binary variables)."""
+    old = os.environ.get("CS_MAX_DENSE_LOG2")
+    os.environ["CS_MAX_DENSE_LOG2"] = "6"
+    try:
+        for d in random_sweep["dbs"][:25]:
+            db = sweep_db(d)
+            s = cs.GpuStrategy(db)
+            for q in d["queries"]:
+                qs = cs.QuerySpec(q["target"], tuple(q["parents"]))
+                col = cs.RecordCollector()
+                s.query(qs, col)
+                assert _recs(col.result()) == golden_records(q)
+                ll = cs.LogLikelihood()
+                s.query(qs, ll)
+                assert rel_close(ll.result(), q["loglik"], 1e-9)
+                sink = cs.NullSink()
+                s.query(qs, sink)
+                assert sink.count == len(q["records"])
+    finally:
+        if old is None:
+            os.environ.pop("CS_MAX_DENSE_LOG2", None)
+        else:
+            os.environ["CS_MAX_DENSE_LOG2"] = old
+    rng = np.random.default_rng(3)
+    data = (rng.random((40, 5000)) < rng.uniform(0.2, 0.8, size=(40, 1))).astype(np.int32)
+    db = cs.Database(data, [2] * 40)
+    s = cs.GpuStrategy(db)
+    qs = cs.QuerySpec(0, tuple(range(1, 40)))
+    col = cs.RecordCollector()
+    s.query(qs, col)
+    want = O.oracle_records(data, db.arities, 0, tuple(range(1, 40)))
+    assert _recs(col.result()) == want
+    ll = cs.LogLikelihood()
+    s.query(qs, ll)
+    assert rel_close(ll.result(), O.loglik_of_records(want), 1e-9)
+    mi = cs.MutualInformation(db.m)
+    s.query(qs, mi)
+    assert abs(mi.result() - O.mi_of_records(want, db.m)) < 1e-9
