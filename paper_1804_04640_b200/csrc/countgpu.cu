@@ -80,8 +80,9 @@ using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32
    {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, false> : nullptr,                           \
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, true> : nullptr},                           \
    {k_hist<K, P_ROWS, false>, k_hist<K, P_ROWS, true>},                                   \
-   {k_hist<K, P_HALF, false>, k_hist<K, P_HALF, true>}}
-static const HistFn kHist[CS_MAXK][5][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
+   {k_hist<K, P_HALF, false>, k_hist<K, P_HALF, true>},                                   \
+   {k_hist<K, P_SLICE, false>, k_hist<K, P_SLICE, true>}}
+static const HistFn kHist[CS_MAXK][6][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
 #undef CS_HK
 
@@ -89,6 +90,7 @@ static int hist_path(const QDesc& d) {
   if (d.pack == 4) return P_PACK4;
   if (d.pack == 2) return P_PACK2;
   if (d.half) return P_HALF;
+  if (d.scells) return P_SLICE;
   return d.mode == 0 ? P_LANE16 : P_ROWS;
 }
 
@@ -622,6 +624,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_half = env_int("CS_HALF", 0) != 0;  // measured slower on cfg2: opt-in
   const bool knob_stages = env_int("CS_STAGES", 1) != 0;
   const bool knob_nibble = env_int("CS_NIBBLE", 1) != 0;
+  const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
   for (int q = 0; q < nq; ++q) {
     const int b = var_off[q], e = var_off[q + 1];
@@ -723,6 +726,14 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           d.rlog = rh;
         }
       }
+    } else if (k >= 2 && c / db->arity[vars[e - 1]] <= smem_words && knob_slice) {
+      // slice class: one CTA per value of the most significant digit, C / r_last cells each
+      d.kind = 0;
+      d.scells = (uint32_t)(c / db->arity[vars[e - 1]]);
+      int rl = 0;
+      while (rl < 5 && ((int64_t)d.scells << (rl + 1)) <= smem_words) ++rl;
+      d.rlog = rl;
+      d.mode = 1;
     } else {
       d.kind = 1;
       d.mode = c <= 65536 ? 1 : 2;
@@ -738,7 +749,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         if (x.half) ct = (ct + 1) / 2;
         return round_up((ct << x.rlog) * 4, 128);
       };
-      if (k <= 4 && knob_stages) {
+      if (k <= 4 && knob_stages && !d.scells) {
         // shrink packing first if it is what keeps the ring from fitting 3 stages
         while (d.pack > 1 && table_bytes(d) + 3 * per_stage > smem_bytes) {
           d.pack = d.pack == 4 ? 2 : 1;
@@ -795,18 +806,30 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     if (d.kind == 1) {
       p->score_list.push_back(q);
       p->needs_global = p->needs_zero = true;
+    } else if (d.scells) {
+      p->score_list.push_back(q);
+      p->needs_global = true;
+      if (nseg > 1) p->needs_zero = true;
     } else if (nseg > 1) {
       p->needs_global = p->needs_zero = true;
     }
+    // slice class: a CTA owns as many consecutive last-digit values as its SMEM holds
+    const int rlast = d.scells ? (int)(d.cells / d.scells) : 1;
+    const int spc = d.scells ? std::max(1, (int)(smem_words / ((int64_t)d.scells << d.rlog))) : 1;
     for (int64_t s = 0; s < nseg; ++s) {
-      WItem w;
-      w.q = q;
-      w.seg = (int32_t)s;
-      w.r0 = s * L;
-      w.r1 = std::min(m, (s + 1) * L);
-      items.push_back(w);
-      const double rows = (double)(w.r1 - w.r0);
-      cost.push_back(rows * (1.0 + d.k) + (d.kind == 0 ? (double)(d.cells << d.rlog) * 2.0 : 0.0));
+      for (int sl = 0; sl < rlast; sl += spc) {
+        WItem w;
+        memset(&w, 0, sizeof w);
+        w.q = q;
+        w.seg = (int32_t)s;
+        w.r0 = s * L;
+        w.r1 = std::min(m, (s + 1) * L);
+        w.slice = sl;
+        w.nsl = std::min(spc, rlast - sl);
+        items.push_back(w);
+        const double rows = (double)(w.r1 - w.r0);
+        cost.push_back(rows * (1.0 + d.k) + (d.kind == 0 ? (double)(d.cells << d.rlog) * 2.0 : 0.0));
+      }
     }
   }
   // longest-processing-time-first order for the persistent CTAs
@@ -837,8 +860,20 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   std::vector<WItem> sorted;
   sorted.reserve(items.size());
   for (int key : keys) {
-    p->groups.push_back({key, (int)sorted.size(), (int)groups[key].size()});
-    for (int i : groups[key]) sorted.push_back(items[i]);
+    auto& g = groups[key];
+    if ((key % 16) / 2 == P_SLICE) {
+      // slices of one segment back to back (they share its columns through L2), queries LPT
+      std::map<int, double> qc;
+      for (int i : g) qc[items[i].q] += cost[i];
+      std::stable_sort(g.begin(), g.end(), [&](int a, int b) {
+        const WItem &x = items[a], &y = items[b];
+        if (x.q != y.q) return qc[x.q] != qc[y.q] ? qc[x.q] > qc[y.q] : x.q < y.q;
+        if (x.seg != y.seg) return x.seg < y.seg;
+        return x.slice < y.slice;
+      });
+    }
+    p->groups.push_back({key, (int)sorted.size(), (int)g.size()});
+    for (int i : g) sorted.push_back(items[i]);
   }
   p->nitems = (int)sorted.size();
   // global class: query-major (all segments of a query back to back, queries LPT by total

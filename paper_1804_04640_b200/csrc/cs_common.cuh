@@ -40,6 +40,7 @@ struct __align__(16) QDesc {
   uint32_t stage_off;           // SMEM class: byte offset of the ring in dynamic SMEM
   int32_t nib;                  // 1: columns read from the 4-bit (nibble) copy, 32 rows / 16 B
   int32_t half;                 // 1: 16-bit counters, two cells per word (hist_smem_half)
+  uint32_t scells;              // slice class: cells per slice (C / arity of the last digit)
 };
 
 // One unit of work: rows [r0, r1) of query q.
@@ -48,6 +49,8 @@ struct WItem {
   int32_t seg;
   int64_t r0;
   int64_t r1;
+  int32_t slice;  // slice class: first value of the last (most significant) digit owned
+  int32_t nsl;    // slice class: number of consecutive last-digit values owned
 };
 
 enum : uint32_t {

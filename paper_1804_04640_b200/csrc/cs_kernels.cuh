@@ -358,6 +358,69 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
 }
 
+// Slice class: tables too large for SMEM but C / r_last <= SMEM capacity.  A CTA owns the
+// slice "last digit == slice" (a contiguous cell range, the last digit being the most
+// significant) and counts only the rows of that slice; the r_last slice-CTAs of a segment are
+// scheduled back to back so the segment's columns come from L2 after the first read.  Index =
+// digits 0..K-2 in 16-bit lanes; the last digit is compared in byte lanes (vcmpeq4) and gates
+// the atomic.  Zero padding rows fall in slice 0, cell 0 and are subtracted there.
+template <int K, bool NIB>
+__device__ __forceinline__ void hist_smem_slice(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
+                                                uint32_t slice, uint32_t nsl) {
+  constexpr int RPV = NIB ? 32 : 16;
+  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  uint32_t co[K], st[K];
+#pragma unroll
+  for (int v = 0; v < K; ++v) {
+    co[v] = q.coff[v];
+    st[v] = q.stride[v];
+  }
+  const int nbyte = q.nbyte < K - 1 ? q.nbyte : K - 1;
+  const int rlog = q.rlog;
+  const uint32_t scale = 4u << rlog;
+  const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
+  char* rbase = reinterpret_cast<char*>(sh) + rep4;
+  const uint32_t s0 = slice * 0x01010101u, ns = nsl * 0x01010101u;
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + RPV - 1) / RPV;
+  auto word = [&](const uint32_t (&w)[K]) {
+    // local last digit d' = d - slice; the row is ours iff d' < nsl (unsigned byte compares)
+    const uint32_t dl = __vsub4(w[K - 1], s0);
+    const uint32_t hit = __vcmpltu4(dl, ns);  // 0xff per row of these slices
+    if (!hit) return;
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K - 1; ++v)
+      if (v < nbyte) a8 += w[v] * st[v];
+    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K - 1; ++v) {
+      if (v >= nbyte) {
+        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      }
+    }
+    // + d' * (cells per slice): local index < nsl * scells <= SMEM capacity < 65536
+    const uint32_t dm = dl & hit;  // zero the lanes of foreign rows (no 16-bit overflow)
+    lo += __byte_perm(dm, 0u, 0x4140) * st[K - 1];
+    hi += __byte_perm(dm, 0u, 0x4342) * st[K - 1];
+    if (hit & 0x000000ffu) atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo & 0xffffu) * scale), 1u);
+    if (hit & 0x0000ff00u) atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo >> 16) * scale), 1u);
+    if (hit & 0x00ff0000u) atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi & 0xffffu) * scale), 1u);
+    if (hit & 0xff000000u) atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi >> 16) * scale), 1u);
+  };
+  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+  for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+    uint32_t a[K][4];
+    load_vec16<K>(a, rowp + (vi << 4), co);
+    cnt(a);
+  }
+  const int64_t pad = nvec * RPV - nrows;
+  if (slice == 0 && pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
+    atomicSub(reinterpret_cast<uint32_t*>(rbase), (uint32_t)pad);
+}
+
 // SMEM class, 16-bit counters (two cells per 32-bit word: cell c lives in word c >> 1, half
 // c & 1, of its replica), which doubles the replica count R that fits -- R = 32 (lane-private,
 // bank-conflict-free) up to 3520 cells instead of 1760.  The host enables it only when a
@@ -628,7 +691,7 @@ __device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0,
 // An SMEM item finishes with the fused epilogue: a single-segment query writes its table and
 // scores straight from SMEM; a multi-segment query adds its partial table into global memory
 // and the last segment to arrive (done counter) scores the merged table.
-enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4 };
+enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4, P_SLICE = 5 };
 constexpr int CS_HIST_THREADS = 1024;
 
 template <int K, int PATH, bool NIB>
@@ -657,7 +720,7 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     const QDesc& q = s_q;
     const int rl = q.rlog;
     const uint32_t R = 1u << rl;
-    const uint32_t C = q.cells;
+    const uint32_t C = PATH == P_SLICE ? q.scells * (uint32_t)wi.nsl : q.cells;
     uint32_t ct = C;  // cells of the SMEM table (C^pack for packed tuples)
     for (int i = 1; i < pack; ++i) ct *= C;
     const uint32_t nw = (PATH == P_HALF ? (C + 1u) >> 1 : ct) << rl;
@@ -668,6 +731,8 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     else if (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
+    else if (PATH == P_SLICE)
+      hist_smem_slice<(K >= 2 ? K : 2), NIB>(q, wi.r0, wi.r1, sh, (uint32_t)wi.slice, (uint32_t)wi.nsl);
     else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {
@@ -708,6 +773,16 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
       __syncthreads();
     }
     auto cell = [&](uint32_t c) -> uint32_t { return compact ? comp[c] : rep_sum(c); };
+    if (PATH == P_SLICE) {
+      // this slice's contiguous cell range; the merged table is scored by the chunked K2
+      uint32_t* t = tables + q.table_off + (uint64_t)wi.slice * q.scells;
+      for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+        const uint32_t v = cell(c);
+        if (q.nseg == 1) t[c] = v;
+        else if (v) atomicAdd(t + c, v);
+      }
+      continue;
+    }
     if (q.nseg == 1) {
       if (tables) {
         uint32_t* t = tables + q.table_off;
