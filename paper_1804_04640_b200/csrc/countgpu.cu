@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <ctime>
 #include <map>
@@ -62,6 +63,12 @@ bool is_device_ptr(const void* p) {
 }
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+double now_ms() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
 
 int env_int(const char* name, int dflt) {
   const char* s = getenv(name);
@@ -605,6 +612,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   if (!db || !out) return fail(CS_ERR_INVALID, "cs_plan_create: NULL argument");
   if (nq < 0) return fail(CS_ERR_INVALID, "cs_plan_create: nq < 0");
   if (nq > 0 && (!var_off || !vars)) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
+  const double trc = now_ms();
   cs_ctx* ctx = db->ctx;
   const int smem_words = ctx->hist_smem / 4;
   const int64_t m = db->m;
@@ -779,11 +787,15 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     total += c;
   }
   p->total_cells = total;
+  const bool trace = env_int("CS_TRACE", 0) != 0;
+  const double tr0 = trace ? now_ms() : 0.0;
   // row segmentation: >= 4 work items per resident CTA, segments of 64K..4M rows
   const int64_t seg_min = 1 << 16, seg_max = knob_seg_max;
   const int64_t target_items = 4LL * ctx->hist_ctas;
   std::vector<WItem> items;
   std::vector<double> cost;
+  items.reserve((size_t)nq * 2);
+  cost.reserve((size_t)nq * 2);
   for (int q = 0; q < nq; ++q) {
     QDesc& d = p->hq[q];
     if (d.kind == 3) {
@@ -832,6 +844,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
     }
   }
+  const double tr1 = trace ? now_ms() : 0.0;
   // longest-processing-time-first order for the persistent CTAs
   std::vector<int> order(items.size());
   std::iota(order.begin(), order.end(), 0);
@@ -839,23 +852,48 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // LPT within a segment.  Concurrently running CTAs then share one row window of the
   // columns, which stays L2-resident (the L2 is split per die, so a 100 MB database does not).
   const bool seg_major = env_int("CS_SEG_ORDER", 1) != 0;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    if (seg_major && items[a].seg != items[b].seg) return items[a].seg < items[b].seg;
-    return cost[a] > cost[b];
-  });
+  {
+    // LPT needs only an approximate cost order: a stable counting sort on (segment, 1/16-octave
+    // cost bucket, descending) is O(items) -- a comparison sort of 10K items cost ~0.7 ms of a
+    // ~4 ms one-shot call
+    constexpr int NB = 1024;
+    int32_t nsegs = 1;
+    for (const WItem& w : items) nsegs = std::max(nsegs, w.seg + 1);
+    if (!seg_major) nsegs = 1;
+    std::vector<int32_t> bucket(items.size());
+    std::vector<int32_t> count((size_t)nsegs * NB + 1, 0);
+    for (size_t i = 0; i < items.size(); ++i) {
+      const int cb = std::max(0, std::min(NB - 1, (int)(std::log2(std::max(cost[i], 1.0)) * 16.0)));
+      bucket[i] = (seg_major ? items[i].seg : 0) * NB + (NB - 1 - cb);
+      count[bucket[i] + 1]++;
+    }
+    for (size_t b = 1; b < count.size(); ++b) count[b] += count[b - 1];
+    for (size_t i = 0; i < items.size(); ++i) order[count[bucket[i]]++] = (int)i;
+  }
   // SMEM-class items grouped by K1 variant (k, path, layout), groups by descending total cost,
   // LPT order inside a group; then the global-class items.
-  std::map<int, std::vector<int>> groups;  // key = (k-1)*16 + path*2 + nib
-  std::map<int, double> gcost;
-  for (size_t i = 0; i < order.size(); ++i) {
-    const QDesc& d = p->hq[items[order[i]].q];
-    if (d.kind != 0) continue;
-    const int key = (d.k - 1) * 16 + hist_path(d) * 2 + d.nib;
-    groups[key].push_back(order[i]);
-    gcost[key] += cost[order[i]];
+  std::vector<std::vector<int>> groups(CS_MAXK * 16);  // key = (k-1)*16 + path*2 + nib
+  std::vector<double> gcost(CS_MAXK * 16, 0.0);
+  {
+    std::vector<int32_t> qkey(nq);
+    std::vector<int32_t> gsize(CS_MAXK * 16, 0);
+    for (int q = 0; q < nq; ++q) {
+      const QDesc& d = p->hq[q];
+      qkey[q] = d.kind == 0 ? (d.k - 1) * 16 + hist_path(d) * 2 + d.nib : -1;
+    }
+    for (const WItem& w : items)
+      if (qkey[w.q] >= 0) gsize[qkey[w.q]]++;
+    for (int k = 0; k < CS_MAXK * 16; ++k) groups[k].reserve(gsize[k]);
+    for (size_t i = 0; i < order.size(); ++i) {
+      const int key = qkey[items[order[i]].q];
+      if (key < 0) continue;
+      groups[key].push_back(order[i]);
+      gcost[key] += cost[order[i]];
+    }
   }
   std::vector<int> keys;
-  for (auto& kv : groups) keys.push_back(kv.first);
+  for (int k = 0; k < (int)groups.size(); ++k)
+    if (!groups[k].empty()) keys.push_back(k);
   std::stable_sort(keys.begin(), keys.end(), [&](int a, int b) { return gcost[a] > gcost[b]; });
   std::vector<WItem> sorted;
   sorted.reserve(items.size());
@@ -895,6 +933,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       for (int i : byq[qq]) sorted.push_back(items[i]);
   }
   p->ngitems = (int)sorted.size() - p->nitems;
+  const double tr2 = trace ? now_ms() : 0.0;
+  if (trace)
+    fprintf(stderr, "plan_build: classify %.3f ms, items %.3f ms, order %.3f ms\n", tr0 - trc, tr1 - tr0,
+            tr2 - tr1);
   // upload descriptors (one blob through pinned staging)
   CS_CUDA(cudaSetDevice(ctx->device));
   const size_t bq = sizeof(QDesc) * std::max(nq, 1);
@@ -950,6 +992,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   p->d_gstride = (uint32_t*)(dblob + ost);
   p->d_head = (int*)(dblob + oh);
   p->d_done = (uint32_t*)(dblob + od);
+  if (trace) fprintf(stderr, "plan_build: upload %.3f ms\n", now_ms() - tr2);
   *out = p;
   return CS_OK;
 }
@@ -1369,16 +1412,11 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
                               int64_t* nnz) {
   cs_plan* p = nullptr;
   const bool trace = env_int("CS_TRACE", 0) != 0;
-  auto now = [] {
-    timespec ts;
-    clock_gettime(CLOCK_MONOTONIC, &ts);
-    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
-  };
-  const double t0 = trace ? now() : 0.0;
+  const double t0 = trace ? now_ms() : 0.0;
   CS_TRY(plan_build(db, nq, var_off, vars, flags, &p, /*transient=*/true));
-  const double t1 = trace ? now() : 0.0;
+  const double t1 = trace ? now_ms() : 0.0;
   int rc = cs_plan_execute(p, tables, loglik, mi, nnz);
-  const double t2 = trace ? now() : 0.0;
+  const double t2 = trace ? now_ms() : 0.0;
   cs_plan_destroy(p);
   if (trace) fprintf(stderr, "cs_query_batch: plan %.3f ms, execute+copy %.3f ms\n", t1 - t0, t2 - t1);
   return rc;

@@ -1,12 +1,17 @@
 // cs_kernels.cuh -- sm_100a kernels of the counting-query engine.
 //
-//   K1 k_hist          batched joint histogram: persistent CTAs pull (query, row-segment)
-//                      work items; 16-row uint4 column loads; mixed-radix joint index in
-//                      SIMD byte / 16-bit lanes; SMEM-privatised, lane-replicated uint32
-//                      tables (conflict-free ATOMS); fused fp64 score epilogue.
+//   K1 k_hist<K,path,layout>  batched joint histogram: persistent CTAs (one per SM) pull
+//                      (query, row segment[, slice]) work items of one variant; 4-bit or uint8
+//                      column vectors (cp.async ring or ld.global.nc.v4); joint index in SIMD
+//                      byte / 16-bit lanes; SMEM-privatised, lane-replicated tables
+//                      (conflict-free ATOMS), packed tuples for tiny tables, slices for tables
+//                      above SMEM capacity; fused fp64 score epilogue.
 //                      Replaces radix._partition_level / radix_query (radix.py:33-156).
+//   K1 k_hist_global   tables above SMEM capacity: RED.ADD into global tables.
+//   K1s k_sparse_*     joint spaces above the dense limit: device hash tables.
 //   K1g k_hist_generic queries with more than CS_MAXK variables (runtime digit loop).
-//   K2 k_score         fp64 LL / MI / nnz over merged global tables (aggregators.py:147-157).
+//   K2 k_score_*       fp64 LL / MI / nnz over merged / global tables, chunked across CTAs
+//                      (aggregators.py:147-157).
 //   K3 k_bitmap_build  per-(variable, state) bit planes (bitmap.py:29-66).
 //   K4 k_points_*      AND + popcount point counts (bitmap.py:131-136) / byte-scan fallback
 //                      when no planes exist (radix.py:181-193 semantics).
@@ -855,17 +860,6 @@ __global__ void k_hist_generic(const QDesc* __restrict__ qd, const int32_t* __re
   }
 }
 
-// K2: scores of global tables, one CTA per listed query.
-__global__ void k_score(const QDesc* __restrict__ qd, const int32_t* __restrict__ qlist,
-                        const uint32_t* __restrict__ tables, double* ll_out, double* mi_out,
-                        int64_t* nnz_out, uint32_t flags, double m_total) {
-  __shared__ ScoreSmem ss;
-  const int q = qlist ? qlist[blockIdx.x] : (int)blockIdx.x;
-  const QDesc& d = qd[q];
-  const uint32_t* t = tables + d.table_off;
-  auto cell = [&](uint32_t c) -> uint32_t { return t[c]; };
-  score_table(cell, d.cells, d.r_target, m_total, flags, q, ll_out, mi_out, nnz_out, ss);
-}
 
 // family scores for the batched learn_parents driver (harness.py:296-348 semantics):
 //   LL(X | Pa) = sum n ln n over joint(X u Pa) - sum n ln n over joint(Pa)
