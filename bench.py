@@ -231,7 +231,9 @@ class QueryRunner:
         self.config = args.config
         self.w, self.queries = workload(args.config, world, rank, args.nq)
         w = self.w
-        self.sharded = args.config == "cfg5" and world > 1
+        # CS_BENCH_FORCE_SHARDED=1 runs the instance-sharded path (CS_PARTIAL + NCCL all-reduce
+        # + cs_plan_score) even at world size 1 -- exercises it on a single-GPU box
+        self.sharded = args.config == "cfg5" and (world > 1 or os.environ.get("CS_BENCH_FORCE_SHARDED") == "1")
         t0 = time.perf_counter()
         if self.sharded:
             from paper_1804_04640_b200.parallel import shard_rows
@@ -484,7 +486,8 @@ def run_ours(args, world, rank, local):
     from paper_1804_04640_b200.engine import GpuContext
 
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = world > 1 or "RANK" in os.environ  # launched by torchrun (even with one rank)
+    if distributed:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -499,7 +502,7 @@ def run_ours(args, world, rank, local):
     for _ in range(args.warmup):
         r.step()
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -518,7 +521,7 @@ def run_ours(args, world, rank, local):
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     step_ms = float(np.mean(ms))
     k_ms = float(np.mean(kernel_ms)) if kernel_ms and min(kernel_ms) > 0 else step_ms
-    if world > 1:
+    if distributed:
         t = torch.tensor([step_ms, k_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         step_ms, k_ms = (float(x) for x in t.tolist())
@@ -526,7 +529,7 @@ def run_ours(args, world, rank, local):
     e2e_ms = []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         r.e2e_step()
@@ -534,7 +537,7 @@ def run_ours(args, world, rank, local):
         if i >= args.warmup:
             e2e_ms.append(dt)
     e2e_step = float(np.mean(e2e_ms))
-    if world > 1:
+    if distributed:
         t = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_step = float(t.item())
@@ -569,7 +572,7 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
 
 

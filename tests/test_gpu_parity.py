@@ -414,3 +414,45 @@ def test_sparse_hash_class(random_sweep):
     mi = cs.MutualInformation(db.m)
     s.query(qs, mi)
     assert abs(mi.result() - O.mi_of_records(want, db.m)) < 1e-9
+
+
+def test_cfg2_full_size_sample(ctx):
+    """configs[1] at full size (m = 1e6): a 200-query sample, bit-exact against the radix
+    restatement on the twin-regenerated columns."""
+    w = workloads.cfg2()
+    gdb = w.build_device(ctx)
+    qs = w.queries[:200]
+    vs = sorted({v for q in qs for v in q})
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m), vs)
+    remap = {v: i for i, v in enumerate(vs)}
+    u8 = np.vstack([cols[v] for v in vs])
+    plan = QueryPlan(gdb, qs, cs._native.CS_WANT_TABLES)
+    tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+    ll = np.zeros(plan.nq)
+    plan.execute(tables=tabs, loglik=ll)
+    otabs, ooff, oll, _ = O.radix_tables(u8, w.arities[vs], [tuple(remap[v] for v in q) for q in qs])
+    assert np.array_equal(tabs, otabs)
+    assert np.allclose(ll, oll, rtol=1e-9, atol=1e-9)
+
+
+def test_cfg4_full_m_sample(ctx):
+    """configs[3] at full m = 1e7: supports of all pairs/triples of 10 of the top items vs the
+    bitmap_count restatement on twin-regenerated columns."""
+    w = workloads.cfg4()
+    gdb = w.build_device(ctx)
+    sup = gdb.count_points([((v,), (1,)) for v in range(w.n)])
+    top = workloads.select_top_items(sup, 200)
+    sample = top[::20]  # 10 items spread over the frequency range
+    gdb.bitmap_build(sample)
+    pr, tr = gdb.itemset_supports(sample)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m), sample)
+    assert [int(sup[v]) for v in sample] == [int(cols[v].sum()) for v in sample]
+    planes = {(v, 1): O.bitmap_planes(cols[v], 1) for v in sample}
+    import itertools
+
+    tri = list(itertools.combinations(range(len(sample)), 3))
+    want = O.bitmap_counts(planes, [tuple((sample[x], 1) for x in t) for t in tri], w.m)
+    assert np.array_equal(tr, want)
+    pairs = list(itertools.combinations(range(len(sample)), 2))
+    wantp = O.bitmap_counts(planes, [((sample[a], 1), (sample[b], 1)) for a, b in pairs], w.m)
+    assert [int(pr[a, b]) for a, b in pairs] == wantp.tolist()
