@@ -270,6 +270,8 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
   c->hist_ctas = per_sm * c->num_sms;
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_itemsets_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               TC_STAGES * TC_STAGE_BYTES));
   *out = c;
   return CS_OK;
 }
@@ -1531,6 +1533,95 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     for (int a = 0; a < b; ++a) rows.push_back(ISRow{(int16_t)a, (int16_t)b});
   }
   const int nrows = (int)rows.size();
+  const int64_t W = db->words;  // multiple of 32 words
+  const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
+  const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
+  static const int use_tc = env_int("CS_ITEMSETS_TC", 1);
+  if (use_tc) {
+    // tensor-core path (K4c): tiles = (128-row block, <=256-column chunk from the block's
+    // smallest b + 1); equal-cost split-K units, LPT over one CTA per SM, each CTA's list in
+    // word order (the SMs sweep the planes together, so a word window stays L2-resident)
+    struct Tile {
+      int row0, col0, ncols;
+    };
+    std::vector<Tile> tiles;
+    double total = 0;
+    for (int r0 = 0; r0 < nrows; r0 += 128) {
+      for (int c0 = rows[r0].b + 1; c0 < n; c0 += TC_NMAX) {
+        const int nc = (int)std::min<int64_t>(TC_NMAX, round_up(n - c0, 16));
+        tiles.push_back(Tile{r0, c0, nc});
+        total += (double)(nc + 48) * W;  // + fixed per-step cost of the A expansion
+      }
+    }
+    const int grid = std::min<int>(ctx->num_sms, std::max<int>(1, (int)tiles.size() * 64));
+    const double target = std::max(total / (grid * 6.0), 64.0 * 8 * 8);
+    std::vector<TCUnit> units;
+    std::vector<double> cost;
+    for (const Tile& t : tiles) {
+      const double tc = (double)(t.ncols + 48) * W;
+      const int64_t pieces = std::max<int64_t>(1, std::min<int64_t>(W / 8, (int64_t)std::ceil(tc / target)));
+      const int64_t step = round_up((W + pieces - 1) / pieces, 8);
+      for (int64_t w0 = 0; w0 < W; w0 += step) {
+        const int64_t w1 = std::min(W, w0 + step);
+        units.push_back(TCUnit{t.row0, (int16_t)t.col0, (int16_t)t.ncols, w0, w1});
+        cost.push_back((double)(t.ncols + 48) * (w1 - w0));
+      }
+    }
+    std::vector<int> order(units.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::vector<std::vector<int>> per(grid);
+    std::vector<std::pair<double, int>> heap;
+    for (int i = 0; i < grid; ++i) heap.emplace_back(0.0, i);
+    auto cmp = [](const std::pair<double, int>& a, const std::pair<double, int>& b) { return a.first > b.first; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (int i : order) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      heap.back().first += cost[i];
+      per[heap.back().second].push_back(i);
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    std::vector<TCUnit> sorted;
+    sorted.reserve(units.size());
+    std::vector<int32_t> cta_off(grid + 1, 0);
+    for (int b = 0; b < grid; ++b) {
+      std::sort(per[b].begin(), per[b].end(), [&](int x, int y) { return units[x].w0 < units[y].w0; });
+      for (int i : per[b]) sorted.push_back(units[i]);
+      cta_off[b + 1] = (int32_t)sorted.size();
+    }
+    const size_t bp = sizeof(void*) * n, br = sizeof(ISRow) * nrows, bu = sizeof(TCUnit) * sorted.size(),
+                 bo = sizeof(int32_t) * cta_off.size();
+    size_t off = 0;
+    auto place = [&](size_t b) {
+      size_t o = off;
+      off = round_up(off + b, 256);
+      return o;
+    };
+    const size_t op = place(bp), orr = place(br), ou = place(bu), oo = place(bo), opr = place(bpairs),
+                 otr = place(btri);
+    void* blob = nullptr;
+    CS_TRY(ctx->scratch_get(10, off, &blob));
+    char* d = (char*)blob;
+    CS_CUDA(cudaMemcpyAsync(d + op, hp.data(), bp, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(d + orr, rows.data(), br, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(d + ou, sorted.data(), bu, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(d + oo, cta_off.data(), bo, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemsetAsync(d + opr, 0, otr - opr + btri, ctx->stream));
+    CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    k_itemsets_tc<<<grid, TC_THREADS, TC_STAGES * TC_STAGE_BYTES, ctx->stream>>>(
+        (const uint32_t* const*)(d + op), (const ISRow*)(d + orr), nrows, n, (const TCUnit*)(d + ou),
+        (const int32_t*)(d + oo), (unsigned long long*)(d + opr), (unsigned long long*)(d + otr));
+    CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->ev_valid = true;
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+    const cudaMemcpyKind kp = is_device_ptr(pairs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const cudaMemcpyKind kt = is_device_ptr(triples) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (pairs) CS_CUDA(cudaMemcpyAsync(pairs, d + opr, bpairs, kp, ctx->stream));
+    if (triples && ntri) CS_CUDA(cudaMemcpyAsync(triples, d + otr, sizeof(uint64_t) * ntri, kt, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CS_OK;
+  }
   std::vector<std::pair<int, int>> tiles;
   for (int r0 = 0; r0 < nrows; r0 += IS_ROWS) {
     const int minb = rows[r0].b;
@@ -1538,7 +1629,6 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     // outputs instead of 1.6x with 32-aligned column blocks
     for (int c0 = minb + 1; c0 < n; c0 += IS_COLS) tiles.emplace_back(r0, c0);
   }
-  const int64_t W = db->words;  // multiple of 32 words
   const int64_t target = 4LL * 2 * ctx->num_sms;
   int64_t S = std::max<int64_t>(1, (target + (int64_t)tiles.size() - 1) / std::max<int64_t>(1, tiles.size()));
   S = std::min<int64_t>(S, W / IS_TW);
@@ -1546,9 +1636,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
   std::vector<ISUnit> units;
   for (int64_t w0 = 0; w0 < W; w0 += slice)
     for (auto& t : tiles) units.push_back(ISUnit{t.first, t.second, w0, std::min(W, w0 + slice)});
-  const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
   const size_t bp = sizeof(void*) * n, br = sizeof(ISRow) * nrows, bu = sizeof(ISUnit) * units.size();
-  const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
   size_t off = 0;
   auto place = [&](size_t b) {
     size_t o = off;

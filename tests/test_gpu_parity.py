@@ -263,6 +263,35 @@ def test_itemset_supports_all_pairs_triples(ctx):
     assert got.tolist() == [int(want_t[triples.index(t)]) for t in sample]
 
 
+def test_itemset_supports_wide_chunked(ctx):
+    """> 256 items: several tensor-core column chunks per row block; ragged m (not a multiple of
+    the 256-row step).  Checked against dense products for a sample of first items a."""
+    rng = np.random.default_rng(23)
+    n, m = 300, 20_011
+    p = np.clip(0.7 * np.arange(1, n + 1) ** -0.3, 0.02, 1.0)
+    u8 = (rng.random((n, m)) < rng.permutation(p)[:, None]).astype(np.uint8)
+    gdb = GpuDatabase.from_columns(ctx, u8, [2] * n)
+    gdb.bitmap_build()
+    pr, tr = gdb.itemset_supports(list(range(n)))
+    x = u8.astype(np.float64)
+    g2 = x @ x.T
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(pr[iu], g2[iu].astype(np.int64))
+
+    def c3(v):
+        return v * (v - 1) * (v - 2) // 6 if v >= 3 else 0
+
+    def c2(v):
+        return v * (v - 1) // 2 if v >= 2 else 0
+
+    for a in (0, 1, 77, 128, 255, 256, 297):
+        t = (x * x[a]) @ x.T  # t[b, c] = support(a, b, c)
+        for b in range(a + 1, n - 1):
+            base = c3(n) - c3(n - a) + c2(n - a - 1) - c2(n - b)
+            got = tr[base:base + (n - b - 1)]
+            assert np.array_equal(got, t[b, b + 1:].astype(np.int64)), (a, b)
+
+
 def test_cfg4_workload_small(ctx):
     """configs[3] generator + top-k selection + supports at reduced m."""
     w = workloads.cfg4(m=200_000, n_items=300, top=40)
