@@ -270,8 +270,6 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
   c->hist_ctas = per_sm * c->num_sms;
-  CS_CUDA(cudaFuncSetAttribute((const void*)k_itemsets_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               TC_STAGES * TC_STAGE_BYTES));
   *out = c;
   return CS_OK;
 }
@@ -1538,88 +1536,246 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
   const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
   static const int use_tc = env_int("CS_ITEMSETS_TC", 1);
   if (use_tc) {
-    // tensor-core path (K4c): tiles = (128-row block, <=256-column chunk from the block's
-    // smallest b + 1); equal-cost split-K units, LPT over one CTA per SM, each CTA's list in
-    // word order (the SMs sweep the planes together, so a word window stays L2-resident)
+    // tensor-core path (K4c, cs_itemsets.cuh).  Tiles = (128-row block, <= 256-column chunk
+    // starting at the block's smallest b + 1).  The step axis is cut into windows whose planes
+    // fit in L2 (~24 MB); inside a window the tiles' costs are laid end to end and cut into one
+    // equal piece per CTA, so every SM works on the same window at the same time.
+    const int64_t nsteps = W / 8;
     struct Tile {
       int row0, col0, ncols;
     };
     std::vector<Tile> tiles;
-    double total = 0;
-    for (int r0 = 0; r0 < nrows; r0 += 128) {
-      for (int c0 = rows[r0].b + 1; c0 < n; c0 += TC_NMAX) {
-        const int nc = (int)std::min<int64_t>(TC_NMAX, round_up(n - c0, 16));
-        tiles.push_back(Tile{r0, c0, nc});
-        total += (double)(nc + 48) * W;  // + fixed per-step cost of the A expansion
+    for (int r0 = 0; r0 < nrows; r0 += 128)
+      for (int c0 = rows[r0].b + 1; c0 < n; c0 += TC_NMAX)
+        tiles.push_back(Tile{r0, c0, (int)std::min<int64_t>(TC_NMAX, round_up(n - c0, 16))});
+    int maxN = 16;
+    for (const Tile& t : tiles) maxN = std::max(maxN, t.ncols);
+    // per row block: the items its rows touch (merged ranges) and each row's two raw slots
+    const int nblocks = (nrows + 127) / 128;
+    std::vector<TCSeg> segs(nblocks);
+    std::vector<TCSlot> slots(nrows);
+    for (int bk = 0; bk < nblocks; ++bk) {
+      std::vector<int> it;
+      for (int r = bk * 128; r < std::min(nrows, bk * 128 + 128); ++r) {
+        it.push_back(rows[r].a);
+        it.push_back(rows[r].b);
       }
-    }
-    const int grid = std::min<int>(ctx->num_sms, std::max<int>(1, (int)tiles.size() * 64));
-    const double target = std::max(total / (grid * 6.0), 64.0 * 8 * 8);
-    std::vector<TCUnit> units;
-    std::vector<double> cost;
-    for (const Tile& t : tiles) {
-      const double tc = (double)(t.ncols + 48) * W;
-      const int64_t pieces = std::max<int64_t>(1, std::min<int64_t>(W / 8, (int64_t)std::ceil(tc / target)));
-      const int64_t step = round_up((W + pieces - 1) / pieces, 8);
-      for (int64_t w0 = 0; w0 < W; w0 += step) {
-        const int64_t w1 = std::min(W, w0 + step);
-        units.push_back(TCUnit{t.row0, (int16_t)t.col0, (int16_t)t.ncols, w0, w1});
-        cost.push_back((double)(t.ncols + 48) * (w1 - w0));
+      std::sort(it.begin(), it.end());
+      it.erase(std::unique(it.begin(), it.end()), it.end());
+      // contiguous copy ranges over the sorted items (one bulk copy per range per step): exact
+      // runs, then the smallest gaps (< 64 items) merged while the copied span stays <= 256 slots
+      // (gap items are copied and ignored)
+      std::vector<std::pair<int, int>> rg;  // [lo, hi]
+      for (size_t k = 0; k < it.size(); ++k) {
+        if (k == 0 || it[k] != it[k - 1] + 1) rg.emplace_back(it[k], it[k]);
+        rg.back().second = it[k];
       }
+      int span = (int)it.size();
+      for (;;) {
+        int best = -1, gap = 64;
+        for (size_t k = 0; k + 1 < rg.size(); ++k) {
+          const int g2 = rg[k + 1].first - rg[k].second - 1;
+          if (g2 < gap && span + g2 <= TC_RAWA / 32) gap = g2, best = (int)k;
+        }
+        if (best < 0) break;
+        span += gap;
+        rg[best].second = rg[best + 1].second;
+        rg.erase(rg.begin() + best + 1);
+      }
+      TCSeg& sg = segs[bk];
+      if ((int)rg.size() > TC_MAXSEG)
+        return fail(CS_ERR_UNSUPPORTED, "itemsets: row block %d has %zu item ranges (max %d)", bk, rg.size(), TC_MAXSEG);
+      sg.nseg = (int)rg.size();
+      for (int k = 0, slot = 0; k < sg.nseg; ++k) {
+        sg.src[k] = rg[k].first;
+        sg.len[k] = rg[k].second - rg[k].first + 1;
+        sg.dst[k] = slot;
+        slot += sg.len[k];
+      }
+      if ((sg.dst[sg.nseg - 1] + sg.len[sg.nseg - 1]) * 32 > TC_RAWA)
+        return fail(CS_ERR_UNSUPPORTED, "itemsets: row block %d spans too many items", bk);
+      auto slot_of = [&](int item) {
+        for (int k = 0; k < sg.nseg; ++k)
+          if (item >= sg.src[k] && item < sg.src[k] + sg.len[k]) return sg.dst[k] + item - sg.src[k];
+        return 0;
+      };
+      for (int r = bk * 128; r < std::min(nrows, bk * 128 + 128); ++r)
+        slots[r] = TCSlot{(int16_t)slot_of(rows[r].a), (int16_t)slot_of(rows[r].b)};
     }
-    std::vector<int> order(units.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-    std::sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    std::vector<std::vector<int>> per(grid);
-    std::vector<std::pair<double, int>> heap;
-    for (int i = 0; i < grid; ++i) heap.emplace_back(0.0, i);
-    auto cmp = [](const std::pair<double, int>& a, const std::pair<double, int>& b) { return a.first > b.first; };
-    std::make_heap(heap.begin(), heap.end(), cmp);
-    for (int i : order) {
-      std::pop_heap(heap.begin(), heap.end(), cmp);
-      heap.back().first += cost[i];
-      per[heap.back().second].push_back(i);
-      std::push_heap(heap.begin(), heap.end(), cmp);
+    // One launch per column-width class (N <= 64, <= 128, <= 256), each with stage geometry
+    // sized for its widest tile: nb operand stages of maxN x 256 B (TMEM A stages packed right
+    // after the accumulator's columns), released in commit groups of cpc stages (a commit costs
+    // short MMAs ~200 issue cycles, tools/microbench6.cu), and a raw ring of nr slots of
+    // (the blocks' item slots + maxN) x 32 B.
+    static int smem_optin = 0;
+    if (!smem_optin) {
+      CS_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+      CS_CUDA(cudaFuncSetAttribute((const void*)k_itemsets_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem_optin - 2048));
     }
-    std::vector<TCUnit> sorted;
-    sorted.reserve(units.size());
-    std::vector<int32_t> cta_off(grid + 1, 0);
-    for (int b = 0; b < grid; ++b) {
-      std::sort(per[b].begin(), per[b].end(), [&](int x, int y) { return units[x].w0 < units[y].w0; });
-      for (int i : per[b]) sorted.push_back(units[i]);
-      cta_off[b + 1] = (int32_t)sorted.size();
+    static const int tc_dbg = env_int("CS_TC_DEBUG", 0);  // diagnostic: skip work per role (wrong results)
+#ifdef CS_TC_PROFILE
+    static const int tc_prof = env_int("CS_TC_PROF", 0);   // diagnostic: per-role wait cycles to stderr
+#else
+    const int tc_prof = 0;  // build with -DCS_TC_PROFILE for per-role wait cycles
+#endif
+    static const double costk = env_int("CS_TC_COSTK", 250);  // fixed per-step cost, in columns (measured)
+    int maxslots = 1;
+    for (const TCSeg& sg : segs) maxslots = std::max(maxslots, sg.dst[sg.nseg - 1] + sg.len[sg.nseg - 1]);
+    const int budget = smem_optin - 2048, rawa_bytes = maxslots * 32;
+    const int grid = ctx->num_sms;
+    const double plane_bytes = 4.0 * (double)W * n;
+    const int64_t nwin = std::max<int64_t>(1, std::min<int64_t>(nsteps / 64, (int64_t)(plane_bytes / 24e6)));
+    struct Launch {
+      size_t unit0;
+      std::vector<int32_t> cta_off;
+      int nb, cpc, a_col, nr, stage_bytes, rawb_bytes, dyn_smem;
+    };
+    std::vector<TCUnit> all_units;
+    std::vector<Launch> launches;
+    static const int tc_classes = env_int("CS_TC_CLASSES", 1);
+    static const int tc_cpc = env_int("CS_TC_CPC", 0);  // 0 = automatic
+    static const int tc_only = env_int("CS_TC_ONLY", 0);
+    static const int tc_sync = env_int("CS_TC_SYNC", 0);  // diagnostic: synchronize after each launch  // diagnostic: launch only class k (1..3)
+    int lo = 0;
+    for (const int hi : {64, 128, 256}) {
+      if (!tc_classes && hi < 256) continue;
+      if (tc_only && hi != (tc_only == 1 ? 64 : tc_only == 2 ? 128 : 256)) {
+        lo = hi;
+        continue;
+      }
+      std::vector<Tile> sub;
+      int maxN = 16;
+      for (const Tile& t : tiles)
+        if (t.ncols > lo && t.ncols <= hi) {
+          sub.push_back(t);
+          maxN = std::max(maxN, t.ncols);
+        }
+      lo = hi;
+      if (sub.empty()) continue;
+      Launch L;
+      L.a_col = (int)round_up(maxN, 64);
+      L.stage_bytes = maxN * TC_KT;
+      L.rawb_bytes = maxN * 32;
+      const int raw_slot = rawa_bytes + L.rawb_bytes;
+      int nb = std::min(TC_MAXNB, (512 - L.a_col) / 64);
+      while (nb > 2 && nb * L.stage_bytes + 6 * raw_slot > budget) --nb;
+      if (nb >= 4) nb &= ~1;
+      L.nb = nb;
+      L.cpc = nb >= 4 ? nb / 2 : 1;
+      if (tc_cpc) L.cpc = nb % tc_cpc == 0 ? tc_cpc : 1;
+      // nr is a multiple of the loader count: raw slot s is then always refilled by the same
+      // loader warp, in order, so its parity waits cannot alias a phase two cycles back (loaders
+      // run independently; with nr % TC_LOADERS != 0 a fast loader could re-arm a slot early)
+      L.nr = std::min(TC_MAXNR, (budget - nb * L.stage_bytes) / raw_slot) / TC_LOADERS * TC_LOADERS;
+      if (L.nr < TC_LOADERS) return fail(CS_ERR_UNSUPPORTED, "itemsets: SMEM plan does not fit (N %d)", maxN);
+      L.dyn_smem = nb * L.stage_bytes + L.nr * raw_slot;
+      // step axis cut into L2-sized windows; inside a window the tiles' costs are laid end to
+      // end and cut into one equal piece per CTA
+      std::vector<std::vector<TCUnit>> per(grid);
+      for (int64_t wi = 0; wi < nwin; ++wi) {
+        const int64_t s0 = nsteps * wi / nwin, s1 = nsteps * (wi + 1) / nwin, len = s1 - s0;
+        if (len <= 0) continue;
+        double T = 0;
+        for (const Tile& t : sub) T += (double)(t.ncols + costk) * len;
+        double C = 0;
+        for (const Tile& t : sub) {
+          const double c = t.ncols + costk;
+          auto cut = [&](int k) {  // step of this tile where CTA k's share begins
+            const double B = T * k / grid;
+            return (int64_t)std::min<double>((double)len, std::max(0.0, std::floor((B - C) / c + 0.5)));
+          };
+          for (int k = std::max(0, (int)std::floor(C * grid / T) - 1); k < grid; ++k) {
+            const int64_t a = cut(k), b = cut(k + 1);
+            if (a >= len) break;
+            if (b > a)
+              per[k].push_back(
+                  TCUnit{t.row0, (int16_t)t.col0, (int16_t)t.ncols, (int32_t)(s0 + a), (int32_t)(s0 + b)});
+          }
+          C += c * len;
+        }
+      }
+      L.unit0 = all_units.size();
+      L.cta_off.assign(grid + 1, 0);
+      for (int b = 0; b < grid; ++b) {
+        for (const TCUnit& u : per[b]) all_units.push_back(u);
+        L.cta_off[b + 1] = (int32_t)(all_units.size() - L.unit0);
+      }
+      launches.push_back(std::move(L));
     }
-    const size_t bp = sizeof(void*) * n, br = sizeof(ISRow) * nrows, bu = sizeof(TCUnit) * sorted.size(),
-                 bo = sizeof(int32_t) * cta_off.size();
+    const size_t bp = sizeof(void*) * n, br = sizeof(ISRow) * nrows, bsl = sizeof(TCSlot) * nrows,
+                 bsg = sizeof(TCSeg) * nblocks, bu = sizeof(TCUnit) * std::max<size_t>(all_units.size(), 1),
+                 bo = sizeof(int32_t) * (grid + 1) * std::max<size_t>(launches.size(), 1),
+                 bpmt = (size_t)nsteps * n * 32;
     size_t off = 0;
     auto place = [&](size_t b) {
       size_t o = off;
       off = round_up(off + b, 256);
       return o;
     };
-    const size_t op = place(bp), orr = place(br), ou = place(bu), oo = place(bo), opr = place(bpairs),
-                 otr = place(btri);
+    const size_t op = place(bp), orr = place(br), osl = place(bsl), osg = place(bsg), ou = place(bu),
+                 oo = place(bo), opr = place(bpairs), otr = place(btri), opm = place(bpmt), opf = place(1024);
     void* blob = nullptr;
     CS_TRY(ctx->scratch_get(10, off, &blob));
     char* d = (char*)blob;
-    CS_CUDA(cudaMemcpyAsync(d + op, hp.data(), bp, cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(d + orr, rows.data(), br, cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(d + ou, sorted.data(), bu, cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(d + oo, cta_off.data(), bo, cudaMemcpyHostToDevice, ctx->stream));
+    // one pinned upload of the plan tables
+    const size_t meta = oo + bo;
+    void* hst = nullptr;
+    CS_TRY(ctx->pinned_get(meta, &hst));
+    char* h = (char*)hst;
+    memcpy(h + op, hp.data(), bp);
+    memcpy(h + orr, rows.data(), br);
+    memcpy(h + osl, slots.data(), bsl);
+    memcpy(h + osg, segs.data(), bsg);
+    if (!all_units.empty()) memcpy(h + ou, all_units.data(), sizeof(TCUnit) * all_units.size());
+    for (size_t li = 0; li < launches.size(); ++li)
+      memcpy(h + oo + sizeof(int32_t) * (grid + 1) * li, launches[li].cta_off.data(), sizeof(int32_t) * (grid + 1));
+    CS_CUDA(cudaMemcpyAsync(d, h, meta, cudaMemcpyHostToDevice, ctx->stream));
     CS_CUDA(cudaMemsetAsync(d + opr, 0, otr - opr + btri, ctx->stream));
+    if (tc_prof) CS_CUDA(cudaMemsetAsync(d + opf, 0, 1024, ctx->stream));
     CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    k_itemsets_tc<<<grid, TC_THREADS, TC_STAGES * TC_STAGE_BYTES, ctx->stream>>>(
-        (const uint32_t* const*)(d + op), (const ISRow*)(d + orr), nrows, n, (const TCUnit*)(d + ou),
-        (const int32_t*)(d + oo), (unsigned long long*)(d + opr), (unsigned long long*)(d + otr));
+    k_pmt_transpose<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((const uint32_t* const*)(d + op), n, nsteps,
+                                                              (uint4*)(d + opm));
+    ctx->launches++;
+    for (size_t li = 0; li < launches.size(); ++li) {
+      const Launch& L = launches[li];
+      k_itemsets_tc<<<grid, TC_THREADS, L.dyn_smem, ctx->stream>>>(
+          (const uint4*)(d + opm), n, (const ISRow*)(d + orr), (const TCSlot*)(d + osl), nrows,
+          (const TCSeg*)(d + osg), (const TCUnit*)(d + ou) + L.unit0,
+          (const int32_t*)(d + oo) + (grid + 1) * li, L.nb, L.cpc, L.a_col, L.nr, L.stage_bytes, rawa_bytes,
+          L.rawb_bytes, (unsigned long long*)(d + opr), (unsigned long long*)(d + otr), tc_dbg,
+          tc_prof ? (long long*)(d + opf) + 16 * li : nullptr);
+      ctx->launches++;
+      if (tc_sync) {
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return fail(CS_ERR_CUDA, "itemsets launch %zu (N<=%d nb %d cpc %d nr %d): %s", li,
+                                          L.stage_bytes / TC_KT, L.nb, L.cpc, L.nr, cudaGetErrorString(e));
+      }
+    }
     CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->ev_valid = true;
-    ctx->launches++;
     CS_CUDA(cudaGetLastError());
     const cudaMemcpyKind kp = is_device_ptr(pairs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     const cudaMemcpyKind kt = is_device_ptr(triples) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (pairs) CS_CUDA(cudaMemcpyAsync(pairs, d + opr, bpairs, kp, ctx->stream));
     if (triples && ntri) CS_CUDA(cudaMemcpyAsync(triples, d + otr, sizeof(uint64_t) * ntri, kt, ctx->stream));
     CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (tc_prof) {
+      long long pr[16 * 3];
+      CS_CUDA(cudaMemcpy(pr, d + opf, sizeof(long long) * 16 * launches.size(), cudaMemcpyDeviceToHost));
+      const double g = grid;
+      for (size_t li = 0; li < launches.size(); ++li) {
+        const long long* q = pr + 16 * li;
+        const Launch& L = launches[li];
+        fprintf(stderr,
+                "[tc prof] launch %zu (N<=%d nb %d cpc %d nr %d units %d): per-CTA Mcycles total avg %.2f max %.2f | "
+                "A wait raw %.2f empty %.2f dfull %.2f epi %.2f | B wait raw %.2f empty %.2f | MMA wait full %.2f "
+                "dempty %.2f issue %.2f | loader wait %.2f issue %.2f\n",
+                li, L.stage_bytes / TC_KT, L.nb, L.cpc, L.nr, L.cta_off[grid], q[11] / g / 1e6, q[12] / 1e6,
+                q[0] / g / 1e6, q[1] / g / 1e6, q[2] / g / 1e6, q[3] / g / 1e6, q[4] / g / 1e6, q[5] / g / 1e6,
+                q[6] / g / 1e6, q[7] / g / 1e6, q[8] / g / 1e6, q[9] / g / 1e6, q[10] / g / 1e6);
+      }
+    }
     return CS_OK;
   }
   std::vector<std::pair<int, int>> tiles;

@@ -180,41 +180,114 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
 // ops per 4 bytes: byte j of 32-bit column 8q + i holds bit 8j + i of the step's word q (both
 // operands use the same permutation, so the dot products are unchanged).
 //
-// Roles (416 threads, one CTA per SM, 512 TMEM columns):
-//   warps 0-3  : A producers (thread t owns TMEM lane t = pair row t), then the epilogue
-//                (tcgen05.ld of the accumulator, 64-bit atomics into pairs / triples)
-//   warps 4-11 : B producers (item planes -> expanded SMEM stage, fence.proxy.async)
-//   warp 12    : MMA issuer (lane 0)
-// Pipelining: TC_STAGES stages; full[s] (384 producer arrivals) -> MMA -> tcgen05.commit ->
-// empty[s]; the last MMA of a unit commits to d_full, the epilogue arrives on d_empty.
-// Units (row block, column chunk, word range) are planned on the host: equal-cost split-K
-// pieces, LPT-assigned per CTA and sorted by word offset so the SMs sweep the planes together.
+// Input: the items' state-1 planes transposed step-major, pmt[step][item] = 32 bytes (one
+// 256-row step of one item; k_pmt_transpose), so every contiguous item range of a step is one
+// contiguous chunk.  A loader thread moves each step's chunks -- the B column range and the
+// row block's merged a/b item segments (TCSeg) -- with cp.async.bulk into a raw ring
+// (mbarrier complete_tx), far ahead of the producers.
+//
+// Roles (one CTA per SM, 512 TMEM columns; G = TC_G producer groups, each taking every G-th
+// step so G per-step latency chains -- raw wait, expansion, tcgen05.st / st.shared, proxy
+// fence, arrive -- are in flight at once):
+//   warps 0 .. 4G-1   : A producers (warp w owns TMEM lanes 32 (w % 4) .. +31 = pair rows),
+//                       then the epilogue (tcgen05.ld of the accumulator, 64-bit atomics into
+//                       pairs / triples; the groups split the columns)
+//   warps 4G .. 8G-1  : B producers (raw item words -> expanded SMEM stage, fence.proxy.async)
+//   warp 8G           : MMA issuer (lane 0)
+//   warps 8G+1 ..     : TC_LOADERS bulk-copy loaders (elected lane; loader j takes steps g % L == j)
+// Pipelines: raw ring raw_full[r] (complete_tx) -> one group's producers -> raw_empty[r];
+// operand stages full[s] (one group's 256 arrivals) -> MMA -> tcgen05.commit -> empty[s]; the last MMA of
+// a unit commits to d_full, the epilogue arrives on d_empty.  Units (row block, column chunk,
+// step range) are planned on the host (cs_itemset_supports): the step axis is cut into
+// L2-sized windows and each window's work is split into equal per-CTA pieces, so all SMs
+// sweep the same window together.
 constexpr int TC_KT = 256;            // data rows (bits) per step = 8 words per plane
-constexpr int TC_STAGES = 3;
 constexpr int TC_NMAX = 256;
-constexpr int TC_STAGE_BYTES = TC_NMAX * TC_KT;  // 64 KB
-constexpr int TC_THREADS = 416;
-constexpr int TC_A_THREADS = 128, TC_B_THREADS = 256;
-constexpr uint32_t TC_A_COL = 256;    // first TMEM column of the A stages (64 columns each)
+#ifndef CS_TC_GROUPS
+#define CS_TC_GROUPS 2
+#endif
+constexpr int TC_G = CS_TC_GROUPS;     // producer groups working on alternate steps
+constexpr int TC_A_THREADS = 128, TC_B_THREADS = 128;  // per group
+constexpr int TC_BT = 2 * TC_NMAX / TC_B_THREADS;       // B tasks per thread per step
+constexpr int TC_LOADERS = 4;          // bulk-copy issuing warps (one issue batch per ~700 cycles
+                                       // per warp, tools/microbench5.cu)
+constexpr int TC_THREADS = TC_G * (TC_A_THREADS + TC_B_THREADS) + 32 + 32 * TC_LOADERS;
+constexpr int TC_RAWA = 256 * 32;     // max raw A bytes per step: <= 256 item slots
+constexpr int TC_MAXSEG = 8;
+constexpr int TC_MAXNB = 8, TC_MAXNR = 16;  // operand stages / raw ring slots (runtime <= these;
+                                            // the host keeps nr a multiple of TC_LOADERS)
+
+// ring position: slot index and the parity of the slot's current phase
+struct TCRing {
+  uint32_t slot = 0, phase = 0;
+  __device__ __forceinline__ void next(uint32_t n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+};
 
 struct TCUnit {
   int32_t row0;   // first pair row (multiple of 128 in the sorted row list)
   int16_t col0;   // first item column
   int16_t ncols;  // N: multiple of 16, <= 256
-  int64_t w0, w1; // word range (multiples of 8)
+  int32_t s0, s1; // step range
 };
+
+struct TCSeg {    // per row block: the items its rows touch, as contiguous ranges
+  int32_t nseg;
+  int32_t src[TC_MAXSEG], len[TC_MAXSEG], dst[TC_MAXSEG];  // item, count, raw slot
+};
+
+struct TCSlot {
+  int16_t sa, sb;  // raw slots of the row's two items
+};
+
+__global__ void k_pmt_transpose(const uint32_t* const* __restrict__ plane, int n, int64_t nsteps,
+                                uint4* __restrict__ pmt) {
+  const int64_t total = nsteps * n * 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int h = (int)(i & 1);
+    const int64_t t = i >> 1;
+    const int item = (int)(t % n);
+    const int64_t st = t / n;
+    pmt[i] = __ldg(reinterpret_cast<const uint4*>(plane[item] + st * 8 + 4 * h));
+  }
+}
 
 __device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// The spin loop lives inside the asm (CUTLASS's pattern): a C loop over an asm output makes
+// the compiler treat everything after it as divergent, which moves every MMA / bulk-copy
+// operand through R2UR on each use.
 __device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TC_WAIT;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// diagnostic wait (-DCS_TC_PROFILE): adds the cycles spent blocked to acc
+__device__ __forceinline__ void tc_wait_t(uint32_t bar, uint32_t parity, long long& acc) {
+#ifdef CS_TC_PROFILE
+  const long long t0 = clock64();
+  tc_wait(bar, parity);
+  acc += clock64() - t0;
+#else
+  tc_wait(bar, parity);
+#endif
+}
+
+__device__ __forceinline__ long long tc_clock() {
+#ifdef CS_TC_PROFILE
+  return clock64();
+#else
+  return 0;
+#endif
 }
 
 __device__ __forceinline__ void tc_arrive(uint32_t bar) {
@@ -245,32 +318,44 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* v) {
       : "memory");
 }
 
-__device__ __forceinline__ uint4 tc_ld4(const uint32_t* p) {
-  return __ldg(reinterpret_cast<const uint4*>(p));
+__device__ __forceinline__ void tc_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_itemsets_tc(const uint32_t* const* __restrict__ plane, const ISRow* __restrict__ rows, int nrows, int n,
-                  const TCUnit* __restrict__ units, const int32_t* __restrict__ cta_off,
-                  unsigned long long* pairs, unsigned long long* triples) {
-  extern __shared__ __align__(16) uint8_t tc_stage[];  // 16 B suffices for SWIZZLE_NONE (and a
+    k_itemsets_tc(const uint4* __restrict__ pmt, int n, const ISRow* __restrict__ rows,
+                  const TCSlot* __restrict__ slots, int nrows, const TCSeg* __restrict__ segs,
+                  const TCUnit* __restrict__ units, const int32_t* __restrict__ cta_off, int nb, int cpc,
+                  int a_col, int nr, int stage_bytes, int rawa_bytes, int rawb_bytes, unsigned long long* pairs,
+                  unsigned long long* triples, int dbg, long long* prof) {
+  extern __shared__ __align__(16) uint8_t tc_smem_buf[];  // 16 B suffices for SWIZZLE_NONE (and a
   // larger alignment here would pad the static SMEM of every kernel in this translation unit)
-  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES], bar_dfull, bar_dempty;
+  __shared__ __align__(8) uint64_t bar_full[TC_MAXNB], bar_empty[TC_MAXNB], bar_rfull[TC_MAXNR],
+      bar_rempty[TC_MAXNR], bar_dfull, bar_dempty;
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long t_start = tc_clock();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(&s_tmem)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < nb; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_full[s])),
                    "r"(TC_A_THREADS + TC_B_THREADS));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_empty[s])), "r"(1));
+      if (s % cpc == 0)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_empty[s / cpc])), "r"(1));
+    }
+    for (int r = 0; r < nr; ++r) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_rfull[r])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_rempty[r])),
+                   "r"(TC_A_THREADS + TC_B_THREADS));
     }
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dfull)), "r"(1));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dempty)), "r"(TC_A_THREADS));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dempty)), "r"(TC_G * TC_A_THREADS));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -278,39 +363,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = s_tmem;
   const int u_begin = cta_off[blockIdx.x], u_end = cta_off[blockIdx.x + 1];
-  const uint32_t stage0 = tc_smem(tc_stage);
+  uint8_t* const stages = tc_smem_buf;
+  uint8_t* const raw = tc_smem_buf + (size_t)nb * stage_bytes;
+  const int raw_bytes = rawa_bytes + rawb_bytes;
 
-  if (warp < 4) {
-    // ---------------- A producers + epilogue ----------------
-    uint32_t g = 0;  // global step counter of this CTA
+  if (warp < 4 * TC_G) {
+    // ---------------- A producers (group grp takes steps g % G == grp) + epilogue ----------------
+    const int grp = warp >> 2, quad = warp & 3, row = quad * 32 + lane;
+    long long pa_raw = 0, pa_empty = 0, pa_dfull = 0, pa_epi = 0;
+    TCRing rr_, sr_;
+    uint32_t g = 0;
     int uc = 0;
     for (int ui = u_begin; ui < u_end; ++ui, ++uc) {
       const TCUnit u = units[ui];
-      const int r = u.row0 + tid;
+      const int r = u.row0 + row;
       const ISRow rr = r < nrows ? rows[r] : ISRow{-1, -1};
-      const uint32_t* pa = rr.a >= 0 ? plane[rr.a] : nullptr;
-      const uint32_t* pb = rr.a >= 0 ? plane[rr.b] : nullptr;
-      uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0;
-      if (pa) {
-        const uint4 a0 = tc_ld4(pa + u.w0), a1 = tc_ld4(pa + u.w0 + 4), b0 = tc_ld4(pb + u.w0),
-                    b1 = tc_ld4(pb + u.w0 + 4);
-        c0 = make_uint4(a0.x & b0.x, a0.y & b0.y, a0.z & b0.z, a0.w & b0.w);
-        c1 = make_uint4(a1.x & b1.x, a1.y & b1.y, a1.z & b1.z, a1.w & b1.w);
-      }
-      for (int64_t w = u.w0; w < u.w1; w += 8, ++g) {
-        uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-        if (pa && w + 8 < u.w1) {
-          const uint4 a0 = tc_ld4(pa + w + 8), a1 = tc_ld4(pa + w + 12), b0 = tc_ld4(pb + w + 8),
-                      b1 = tc_ld4(pb + w + 12);
-          n0 = make_uint4(a0.x & b0.x, a0.y & b0.y, a0.z & b0.z, a0.w & b0.w);
-          n1 = make_uint4(a1.x & b1.x, a1.y & b1.y, a1.z & b1.z, a1.w & b1.w);
-        }
-        const uint32_t s = g % TC_STAGES;
-        tc_wait(tc_smem(&bar_empty[s]), ((g / TC_STAGES) & 1) ^ 1);
-        const uint32_t x[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + TC_A_COL + s * 64;
+      const TCSlot sl = r < nrows ? slots[r] : TCSlot{0, 0};
+      for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
+        if ((int)(g % TC_G) != grp) continue;
+        tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pa_raw);
+        const uint8_t* ra = raw + (size_t)rr_.slot * raw_bytes;
+        const uint4 a0 = *reinterpret_cast<const uint4*>(ra + sl.sa * 32);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(ra + sl.sa * 32 + 16);
+        const uint4 b0 = *reinterpret_cast<const uint4*>(ra + sl.sb * 32);
+        const uint4 b1 = *reinterpret_cast<const uint4*>(ra + sl.sb * 32 + 16);
+        tc_arrive(tc_smem(&bar_rempty[rr_.slot]));
+        const uint32_t x[8] = {a0.x & b0.x, a0.y & b0.y, a0.z & b0.z, a0.w & b0.w,
+                               a1.x & b1.x, a1.y & b1.y, a1.z & b1.z, a1.w & b1.w};
+        tc_wait_t(tc_smem(&bar_empty[sr_.slot / cpc]), sr_.phase ^ 1, pa_empty);
+        // order the stage's TMEM stores after the MMAs that read it (released by the commit)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + a_col + sr_.slot * 64;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
+          if (dbg & 4) break;
           uint32_t v[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -321,15 +407,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        tc_arrive(tc_smem(&bar_full[s]));
-        c0 = n0;
-        c1 = n1;
+        tc_arrive(tc_smem(&bar_full[sr_.slot]));
       }
-      // epilogue: accumulator lane tid = pair row, columns 0..ncols-1 = items col0..
-      tc_wait(tc_smem(&bar_dfull), uc & 1);
+      // epilogue: accumulator lane = pair row, columns 0..ncols-1 = items col0..; the groups
+      // split the 16-column chunks
+      tc_wait_t(tc_smem(&bar_dfull), uc & 1, pa_dfull);
+      const long long te0 = tc_clock();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t td = tmem + ((uint32_t)(warp * 32) << 16);
-      for (int j0 = 0; j0 < u.ncols; j0 += 16) {
+      const uint32_t td = tmem + ((uint32_t)(quad * 32) << 16);
+      for (int j0 = 16 * grp; j0 < u.ncols; j0 += 16 * TC_G) {
         uint32_t v[16];
         tc_ld16(td + j0, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -344,44 +430,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       tc_arrive(tc_smem(&bar_dempty));
+      pa_epi += tc_clock() - te0;
     }
-  } else if (warp < 12) {
+    if (prof && lane == 0 && warp == 0) {
+      atomicAdd((unsigned long long*)&prof[0], (unsigned long long)pa_raw);
+      atomicAdd((unsigned long long*)&prof[1], (unsigned long long)pa_empty);
+      atomicAdd((unsigned long long*)&prof[2], (unsigned long long)pa_dfull);
+      atomicAdd((unsigned long long*)&prof[3], (unsigned long long)pa_epi);
+    }
+  } else if (warp < 8 * TC_G) {
     // ---------------- B producers ----------------
-    const int bt = tid - TC_A_THREADS;
+    const int grp = (warp - 4 * TC_G) >> 2, bt = tid - 32 * 4 * TC_G - TC_B_THREADS * grp;
+    long long pb_raw = 0, pb_empty = 0;
+    TCRing rr_, sr_;
     uint32_t g = 0;
     for (int ui = u_begin; ui < u_end; ++ui) {
       const TCUnit u = units[ui];
       const int N = u.ncols;
-      // tasks e = bt, bt + 256 over (item il = e % N, half h = e / N): 4 words -> 32 bytes x 4
-      const uint32_t* src[2];
-      uint32_t dst[2];
-      int h4[2];
+      // tasks e = bt + 128 k over (item il = e % N, half h = e / N): 4 words -> 4 x 32 bytes
+      int roff[TC_BT], h4[TC_BT];
+      uint32_t dst[TC_BT];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < TC_BT; ++k) {
         const int e = bt + TC_B_THREADS * k;
-        src[k] = nullptr;
         dst[k] = 0xffffffffu;
-        h4[k] = 0;
+        roff[k] = h4[k] = 0;
         if (e < 2 * N) {
-          const int il = e % N, h = e / N, item = u.col0 + il;
+          const int il = e % N, h = e / N;
           h4[k] = 4 * h;
+          roff[k] = rawa_bytes + il * 32 + 16 * h;
           dst[k] = (uint32_t)((il >> 3) * 2048 + (il & 7) * 16);
-          if (item < n) src[k] = plane[item] + 4 * h;
         }
       }
-      uint4 cur[2], nxt[2];
+      for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
+        if ((int)(g % TC_G) != grp) continue;
+        tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pb_raw);
+        const uint8_t* rb = raw + (size_t)rr_.slot * raw_bytes;
+        uint4 cur[TC_BT];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) cur[k] = src[k] ? tc_ld4(src[k] + u.w0) : make_uint4(0, 0, 0, 0);
-      for (int64_t w = u.w0; w < u.w1; w += 8, ++g) {
+        for (int k = 0; k < TC_BT; ++k)
+          if (dst[k] != 0xffffffffu) cur[k] = *reinterpret_cast<const uint4*>(rb + roff[k]);
+        tc_arrive(tc_smem(&bar_rempty[rr_.slot]));
+        tc_wait_t(tc_smem(&bar_empty[sr_.slot / cpc]), sr_.phase ^ 1, pb_empty);
+        uint8_t* sp = stages + (size_t)sr_.slot * stage_bytes;
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-          nxt[k] = (src[k] && w + 8 < u.w1) ? tc_ld4(src[k] + w + 8) : make_uint4(0, 0, 0, 0);
-        const uint32_t s = g % TC_STAGES;
-        tc_wait(tc_smem(&bar_empty[s]), ((g / TC_STAGES) & 1) ^ 1);
-        uint8_t* st = tc_stage + (size_t)s * TC_STAGE_BYTES;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          if (dst[k] == 0xffffffffu) continue;
+        for (int k = 0; k < TC_BT; ++k) {
+          if (dst[k] == 0xffffffffu || (dbg & 8)) continue;
           const uint32_t x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
@@ -395,54 +489,154 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             hi.y = (x[qq] >> 5) & 0x01010101u;
             hi.z = (x[qq] >> 6) & 0x01010101u;
             hi.w = (x[qq] >> 7) & 0x01010101u;
-            *reinterpret_cast<uint4*>(st + dst[k] + (2 * q) * 128) = lo;
-            *reinterpret_cast<uint4*>(st + dst[k] + (2 * q + 1) * 128) = hi;
+            *reinterpret_cast<uint4*>(sp + dst[k] + (2 * q) * 128) = lo;
+            *reinterpret_cast<uint4*>(sp + dst[k] + (2 * q + 1) * 128) = hi;
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_arrive(tc_smem(&bar_full[s]));
-        cur[0] = nxt[0];
-        cur[1] = nxt[1];
+        tc_arrive(tc_smem(&bar_full[sr_.slot]));
       }
     }
-  } else if (lane == 0) {
+    if (prof && bt == 0 && grp == 0) {
+      atomicAdd((unsigned long long*)&prof[4], (unsigned long long)pb_raw);
+      atomicAdd((unsigned long long*)&prof[5], (unsigned long long)pb_empty);
+    }
+  } else if (warp == 8 * TC_G) {
     // ---------------- MMA issuer ----------------
-    uint32_t g = 0;
-    int uc = 0;
+    // The whole warp runs the loop (its operands stay warp-uniform, in uniform registers) and
+    // one elected lane issues; a single divergent lane would move every operand through
+    // R2UR per instruction (~100 cycles per MMA, measured).
+    TCRing sr_;
+    int uc = 0, gsub = 0, gidx = 0;  // position inside the current commit group / group index
+    long long pm_full = 0, pm_dempty = 0, pm_issue = 0;
+    const uint32_t stage0 = tc_smem(stages);
+    const uint64_t sdesc0 = tc_sdesc(stage0);
     for (int ui = u_begin; ui < u_end; ++ui, ++uc) {
-      const TCUnit u = units[ui];
+      const int ncols = __shfl_sync(0xffffffffu, (int)units[ui].ncols, 0);
+      const int s0 = __shfl_sync(0xffffffffu, units[ui].s0, 0), s1 = __shfl_sync(0xffffffffu, units[ui].s1, 0);
       // idesc: D s32 (bits 4-5 = 2), A/B u8, K-major, N >> 3 at bit 17, M >> 4 at bit 24
-      const uint32_t idesc = (2u << 4) | ((uint32_t)(u.ncols >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-      tc_wait(tc_smem(&bar_dempty), (uc & 1) ^ 1);
+      const uint32_t idesc = (2u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      tc_wait_t(tc_smem(&bar_dempty), (uc & 1) ^ 1, pm_dempty);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      bool first = true;
-      for (int64_t w = u.w0; w < u.w1; w += 8, ++g) {
-        const uint32_t s = g % TC_STAGES;
-        tc_wait(tc_smem(&bar_full[s]), (g / TC_STAGES) & 1);
+      uint32_t acc0 = 0;
+      for (int st = s0; st < s1; ++st) {
+        tc_wait_t(tc_smem(&bar_full[sr_.slot]), sr_.phase, pm_full);
+        const long long ti0 = tc_clock();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ta = tmem + TC_A_COL + s * 64;
-        const uint32_t sb = stage0 + s * TC_STAGE_BYTES;
-#pragma unroll
-        for (int j = 0; j < TC_KT / 32; ++j) {
-          const uint32_t acc = (first && j == 0) ? 0u : 1u;
+        const uint32_t ta = tmem + a_col + sr_.slot * 64;
+        // descriptor start address advances 256 B (16 in 16-byte units) per K = 32 slice
+        const uint64_t db = sdesc0 + (uint64_t)((sr_.slot * (uint32_t)stage_bytes) >> 4);
+        if (!(dbg & 2))
           asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
-              "r"(ta + 8u * j), "l"(tc_sdesc(sb + 256u * j)), "r"(idesc), "r"(acc)
+              "{\n\t.reg .pred e, p;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%5], %6, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%7], %8, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%9], %10, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%11], %12, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%13], %14, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%15], %16, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%17], %18, %3, 1;\n\t}" ::"r"(tmem),
+              "r"(ta), "l"(db), "r"(idesc), "r"(acc0), "r"(ta + 8), "l"(db + 16), "r"(ta + 16), "l"(db + 32),
+              "r"(ta + 24), "l"(db + 48), "r"(ta + 32), "l"(db + 64), "r"(ta + 40), "l"(db + 80), "r"(ta + 48),
+              "l"(db + 96), "r"(ta + 56), "l"(db + 112)
               : "memory");
+        // one commit per group of cpc stages (a commit stalls the issue of short MMAs by ~200
+        // cycles, tools/microbench6.cu)
+        if (++gsub == cpc) {
+          asm volatile(
+              "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                  tc_smem(&bar_empty[gidx]))
+              : "memory");
+          gsub = 0;
+          if (++gidx == nb / cpc) gidx = 0;
         }
-        first = false;
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         tc_smem(&bar_empty[s]))
-                     : "memory");
+        acc0 = 1;
+        sr_.next(nb);
+        pm_issue += tc_clock() - ti0;
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       tc_smem(&bar_dfull))
-                   : "memory");
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+              tc_smem(&bar_dfull))
+          : "memory");
+    }
+    if (prof && lane == 0) {
+      atomicAdd((unsigned long long*)&prof[6], (unsigned long long)pm_full);
+      atomicAdd((unsigned long long*)&prof[7], (unsigned long long)pm_dempty);
+      atomicAdd((unsigned long long*)&prof[8], (unsigned long long)pm_issue);
+    }
+  } else {
+    // ---------------- bulk-copy loaders (whole warps, elected issue; loader j takes steps g % L == j) --------
+    const int lw = warp - 8 * TC_G - 1;
+    TCRing rr_;
+    uint32_t g = 0;
+    long long pl_empty = 0, pl_issue = 0;
+    const uint32_t raw0 = tc_smem(raw);
+    for (int ui = u_begin; ui < u_end; ++ui) {
+      const int row0 = __shfl_sync(0xffffffffu, units[ui].row0, 0);
+      const int col0 = __shfl_sync(0xffffffffu, (int)units[ui].col0, 0);
+      const int ncols = __shfl_sync(0xffffffffu, (int)units[ui].ncols, 0);
+      const int s0 = __shfl_sync(0xffffffffu, units[ui].s0, 0), s1 = __shfl_sync(0xffffffffu, units[ui].s1, 0);
+      const TCSeg& sg = segs[row0 / 128];
+      uint32_t soff[TC_MAXSEG], doff[TC_MAXSEG], nby[TC_MAXSEG];
+      uint32_t bytes = 0;
+#pragma unroll
+      for (int k = 0; k < TC_MAXSEG; ++k) {
+        const bool on = k < sg.nseg;
+        soff[k] = on ? 32u * sg.src[k] : 0u;
+        doff[k] = on ? 32u * sg.dst[k] : 0u;
+        nby[k] = on ? 32u * sg.len[k] : 0u;
+        bytes += nby[k];
+      }
+      const uint32_t nbb = 32u * (uint32_t)min(ncols, n - col0);
+      bytes += nbb;
+      for (int st = s0; st < s1; ++st, ++g, rr_.next(nr)) {
+        if ((int)(g % TC_LOADERS) != lw) continue;
+        tc_wait_t(tc_smem(&bar_rempty[rr_.slot]), rr_.phase ^ 1, pl_empty);
+        const long long tl0 = tc_clock();
+        const uint32_t bar = tc_smem(&bar_rfull[rr_.slot]);
+        const char* base = reinterpret_cast<const char*>(pmt) + (int64_t)st * n * 32;
+        const uint32_t rdst = raw0 + rr_.slot * raw_bytes;
+        if (dbg & 1) {
+          if (lane == 0) tc_arrive(bar);
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred e, p;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+              "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n\t"
+              "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%5], [%6], %7, [%0];\n\t"
+              "setp.ne.and.u32 p, %10, 0, e;\n\t"
+              "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%9], %10, [%0];\n\t"
+              "setp.ne.and.u32 p, %13, 0, e;\n\t"
+              "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%11], [%12], %13, [%0];\n\t"
+              "}" ::"r"(bar),
+              "r"(bytes), "r"(rdst + (uint32_t)rawa_bytes), "l"(base + 32 * col0), "r"(nbb), "r"(rdst + doff[0]),
+              "l"(base + soff[0]), "r"(nby[0]), "r"(rdst + doff[1]), "l"(base + soff[1]), "r"(nby[1]),
+              "r"(rdst + doff[2]), "l"(base + soff[2]), "r"(nby[2])
+              : "memory");
+#pragma unroll
+          for (int k = 3; k < TC_MAXSEG; ++k)
+            if (nby[k] && lane == 0) tc_bulk(rdst + doff[k], base + soff[k], nby[k], bar);
+        }
+        pl_issue += tc_clock() - tl0;
+      }
+    }
+    if (prof && lane == 0 && lw == 0) {
+      atomicAdd((unsigned long long*)&prof[9], (unsigned long long)pl_empty);
+      atomicAdd((unsigned long long*)&prof[10], (unsigned long long)pl_issue);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (prof && tid == 0) {
+    atomicAdd((unsigned long long*)&prof[11], (unsigned long long)(tc_clock() - t_start));
+    atomicMax((unsigned long long*)&prof[12], (unsigned long long)(tc_clock() - t_start));
+  }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
