@@ -1629,7 +1629,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     struct Launch {
       size_t unit0;
       std::vector<int32_t> cta_off;
-      int nb, cpc, a_col, nr, stage_bytes, rawb_bytes, dyn_smem;
+      int ga, nb, cpc, a_col, nr, stage_bytes, rawb_bytes, dyn_smem;
     };
     std::vector<TCUnit> all_units;
     std::vector<Launch> launches;
@@ -1659,14 +1659,19 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
       L.rawb_bytes = maxN * 32;
       const int raw_slot = rawa_bytes + L.rawb_bytes;
       int nb = std::min(TC_MAXNB, (512 - L.a_col) / 64);
+      // nb >= the B group count; the A group count ga <= nb (parity waits on the stage ring stay
+      // unambiguous when a group's previous step is at least nb steps back)
       while (nb > 2 && nb * L.stage_bytes + 6 * raw_slot > budget) --nb;
       if (nb >= 4) nb &= ~1;
       L.nb = nb;
+      L.ga = std::min(TC_GA, nb >= 4 ? 4 : 2);  // divides nr (a multiple of 4): raw-slot parity waits stay unambiguous
       L.cpc = nb >= 4 ? nb / 2 : 1;
       if (tc_cpc) L.cpc = nb % tc_cpc == 0 ? tc_cpc : 1;
-      // nr is a multiple of the loader count: raw slot s is then always refilled by the same
+      // nr is a multiple of the loader count (4): raw slot s is then always refilled by the same
       // loader warp, in order, so its parity waits cannot alias a phase two cycles back (loaders
-      // run independently; with nr % TC_LOADERS != 0 a fast loader could re-arm a slot early)
+      // run independently; with nr % TC_LOADERS != 0 a fast loader could re-arm a slot early).
+      // It is also a multiple of the A / B group counts, so a slot's consumers are always the
+      // same groups, which have consumed its previous fill.
       L.nr = std::min(TC_MAXNR, (budget - nb * L.stage_bytes) / raw_slot) / TC_LOADERS * TC_LOADERS;
       if (L.nr < TC_LOADERS) return fail(CS_ERR_UNSUPPORTED, "itemsets: SMEM plan does not fit (N %d)", maxN);
       L.dyn_smem = nb * L.stage_bytes + L.nr * raw_slot;
@@ -1742,7 +1747,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
       k_itemsets_tc<<<grid, TC_THREADS, L.dyn_smem, ctx->stream>>>(
           (const uint4*)(d + opm), n, (const ISRow*)(d + orr), (const TCSlot*)(d + osl), nrows,
           (const TCSeg*)(d + osg), (const TCUnit*)(d + ou) + L.unit0,
-          (const int32_t*)(d + oo) + (grid + 1) * li, L.nb, L.cpc, L.a_col, L.nr, L.stage_bytes, rawa_bytes,
+          (const int32_t*)(d + oo) + (grid + 1) * li, L.ga, L.nb, L.cpc, L.a_col, L.nr, L.stage_bytes, rawa_bytes,
           L.rawb_bytes, (unsigned long long*)(d + opr), (unsigned long long*)(d + otr), tc_dbg,
           tc_prof ? (long long*)(d + opf) + 16 * li : nullptr);
       ctx->launches++;
@@ -1769,10 +1774,11 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
         const Launch& L = launches[li];
         fprintf(stderr,
                 "[tc prof] launch %zu (N<=%d nb %d cpc %d nr %d units %d): per-CTA Mcycles total avg %.2f max %.2f | "
-                "A wait raw %.2f empty %.2f dfull %.2f epi %.2f | B wait raw %.2f empty %.2f | MMA wait full %.2f "
-                "dempty %.2f issue %.2f | loader wait %.2f issue %.2f\n",
+                "A wait raw %.2f empty %.2f dfull %.2f epi %.2f lds %.2f st %.2f | B wait raw %.2f empty %.2f | "
+                "MMA wait full %.2f dempty %.2f issue %.2f | loader wait %.2f issue %.2f\n",
                 li, L.stage_bytes / TC_KT, L.nb, L.cpc, L.nr, L.cta_off[grid], q[11] / g / 1e6, q[12] / 1e6,
-                q[0] / g / 1e6, q[1] / g / 1e6, q[2] / g / 1e6, q[3] / g / 1e6, q[4] / g / 1e6, q[5] / g / 1e6,
+                q[0] / g / 1e6, q[1] / g / 1e6, q[2] / g / 1e6, q[3] / g / 1e6, q[13] / g / 1e6, q[14] / g / 1e6,
+                q[4] / g / 1e6, q[5] / g / 1e6,
                 q[6] / g / 1e6, q[7] / g / 1e6, q[8] / g / 1e6, q[9] / g / 1e6, q[10] / g / 1e6);
       }
     }

@@ -186,15 +186,16 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
 // row block's merged a/b item segments (TCSeg) -- with cp.async.bulk into a raw ring
 // (mbarrier complete_tx), far ahead of the producers.
 //
-// Roles (one CTA per SM, 512 TMEM columns; G = TC_G producer groups, each taking every G-th
-// step so G per-step latency chains -- raw wait, expansion, tcgen05.st / st.shared, proxy
-// fence, arrive -- are in flight at once):
-//   warps 0 .. 4G-1   : A producers (warp w owns TMEM lanes 32 (w % 4) .. +31 = pair rows),
-//                       then the epilogue (tcgen05.ld of the accumulator, 64-bit atomics into
-//                       pairs / triples; the groups split the columns)
-//   warps 4G .. 8G-1  : B producers (raw item words -> expanded SMEM stage, fence.proxy.async)
-//   warp 8G           : MMA issuer (lane 0)
-//   warps 8G+1 ..     : TC_LOADERS bulk-copy loaders (elected lane; loader j takes steps g % L == j)
+// Roles (one CTA per SM, 512 TMEM columns).  Producer groups take interleaved steps so several
+// per-step latency chains are in flight: an A group's chain is dominated by the completion of
+// its tcgen05.st (~800 cycles measured), so up to TC_GA = 4 A groups run (ga <= nb per launch,
+// which keeps the stage ring's parity waits unambiguous); TC_GB = 2 B groups.
+//   warps 0 .. 4GA-1          : A producers (warp w owns TMEM lanes 32 (w % 4) .. +31 = pair
+//                               rows), then the epilogue (tcgen05.ld of the accumulator, 64-bit
+//                               atomics into pairs / triples; the groups split the columns)
+//   warps 4GA .. 4(GA+GB)-1   : B producers (raw item words -> expanded SMEM stage, fence.proxy.async)
+//   warp 4(GA+GB)             : MMA issuer (whole warp, elected lane)
+//   warps 4(GA+GB)+1 ..       : TC_LOADERS bulk-copy loaders (elected lane; loader j takes steps g % L == j)
 // Pipelines: raw ring raw_full[r] (complete_tx) -> one group's producers -> raw_empty[r];
 // operand stages full[s] (one group's 256 arrivals) -> MMA -> tcgen05.commit -> empty[s]; the last MMA of
 // a unit commits to d_full, the epilogue arrives on d_empty.  Units (row block, column chunk,
@@ -203,15 +204,13 @@ __global__ void __launch_bounds__(IS_THREADS, 2)
 // sweep the same window together.
 constexpr int TC_KT = 256;            // data rows (bits) per step = 8 words per plane
 constexpr int TC_NMAX = 256;
-#ifndef CS_TC_GROUPS
-#define CS_TC_GROUPS 2
-#endif
-constexpr int TC_G = CS_TC_GROUPS;     // producer groups working on alternate steps
+constexpr int TC_GA = 2;  // A producer groups (4 warps each; per launch ga <= min(TC_GA, nb) are used)
+constexpr int TC_GB = 2;  // B producer groups (4 warps each)
 constexpr int TC_A_THREADS = 128, TC_B_THREADS = 128;  // per group
 constexpr int TC_BT = 2 * TC_NMAX / TC_B_THREADS;       // B tasks per thread per step
 constexpr int TC_LOADERS = 4;          // bulk-copy issuing warps (one issue batch per ~700 cycles
                                        // per warp, tools/microbench5.cu)
-constexpr int TC_THREADS = TC_G * (TC_A_THREADS + TC_B_THREADS) + 32 + 32 * TC_LOADERS;
+constexpr int TC_THREADS = TC_GA * TC_A_THREADS + TC_GB * TC_B_THREADS + 32 + 32 * TC_LOADERS;
 constexpr int TC_RAWA = 256 * 32;     // max raw A bytes per step: <= 256 item slots
 constexpr int TC_MAXSEG = 8;
 constexpr int TC_MAXNB = 8, TC_MAXNR = 16;  // operand stages / raw ring slots (runtime <= these;
@@ -294,6 +293,14 @@ __device__ __forceinline__ void tc_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// one arrival per warp: each lane has ordered its own accesses (fences) before this point;
+// __syncwarp orders them before lane 0's release-arrive.  256 per-thread arrivals on one SMEM
+// word per step serialised the producers (measured ~1400 cycles per step).
+__device__ __forceinline__ void tc_arrive_warp(uint32_t bar, int lane) {
+  __syncwarp();
+  if (lane == 0) tc_arrive(bar);
+}
+
 __device__ __forceinline__ uint64_t tc_sdesc(uint32_t addr) {
   // K-major, no swizzle: LBO = 128 B (next 16-byte K chunk), SBO = 2048 B (next 8-row group)
   return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(2048 >> 4) << 32) |
@@ -327,7 +334,7 @@ __device__ __forceinline__ void tc_bulk(uint32_t dst, const void* src, uint32_t 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_itemsets_tc(const uint4* __restrict__ pmt, int n, const ISRow* __restrict__ rows,
                   const TCSlot* __restrict__ slots, int nrows, const TCSeg* __restrict__ segs,
-                  const TCUnit* __restrict__ units, const int32_t* __restrict__ cta_off, int nb, int cpc,
+                  const TCUnit* __restrict__ units, const int32_t* __restrict__ cta_off, int ga, int nb, int cpc,
                   int a_col, int nr, int stage_bytes, int rawa_bytes, int rawb_bytes, unsigned long long* pairs,
                   unsigned long long* triples, int dbg, long long* prof) {
   extern __shared__ __align__(16) uint8_t tc_smem_buf[];  // 16 B suffices for SWIZZLE_NONE (and a
@@ -345,17 +352,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (tid == 32) {
     for (int s = 0; s < nb; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_full[s])),
-                   "r"(TC_A_THREADS + TC_B_THREADS));
+                   "r"((TC_A_THREADS + TC_B_THREADS) / 32));
       if (s % cpc == 0)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_empty[s / cpc])), "r"(1));
     }
     for (int r = 0; r < nr; ++r) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_rfull[r])), "r"(1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_rempty[r])),
-                   "r"(TC_A_THREADS + TC_B_THREADS));
+                   "r"((TC_A_THREADS + TC_B_THREADS) / 32));
     }
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dfull)), "r"(1));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dempty)), "r"(TC_G * TC_A_THREADS));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem(&bar_dempty)), "r"(TC_GA * TC_A_THREADS / 32));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -367,10 +374,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* const raw = tc_smem_buf + (size_t)nb * stage_bytes;
   const int raw_bytes = rawa_bytes + rawb_bytes;
 
-  if (warp < 4 * TC_G) {
+  if (warp < 4 * TC_GA) {
     // ---------------- A producers (group grp takes steps g % G == grp) + epilogue ----------------
     const int grp = warp >> 2, quad = warp & 3, row = quad * 32 + lane;
-    long long pa_raw = 0, pa_empty = 0, pa_dfull = 0, pa_epi = 0;
+    long long pa_raw = 0, pa_empty = 0, pa_dfull = 0, pa_epi = 0, pa_st = 0, pa_lds = 0;
     TCRing rr_, sr_;
     uint32_t g = 0;
     int uc = 0;
@@ -380,20 +387,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const ISRow rr = r < nrows ? rows[r] : ISRow{-1, -1};
       const TCSlot sl = r < nrows ? slots[r] : TCSlot{0, 0};
       for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
-        if ((int)(g % TC_G) != grp) continue;
+        if ((int)(g % ga) != grp) continue;
         tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pa_raw);
+        const long long tq0 = tc_clock();
         const uint8_t* ra = raw + (size_t)rr_.slot * raw_bytes;
         const uint4 a0 = *reinterpret_cast<const uint4*>(ra + sl.sa * 32);
         const uint4 a1 = *reinterpret_cast<const uint4*>(ra + sl.sa * 32 + 16);
         const uint4 b0 = *reinterpret_cast<const uint4*>(ra + sl.sb * 32);
         const uint4 b1 = *reinterpret_cast<const uint4*>(ra + sl.sb * 32 + 16);
-        tc_arrive(tc_smem(&bar_rempty[rr_.slot]));
+        tc_arrive_warp(tc_smem(&bar_rempty[rr_.slot]), lane);
+        pa_lds += tc_clock() - tq0;
         const uint32_t x[8] = {a0.x & b0.x, a0.y & b0.y, a0.z & b0.z, a0.w & b0.w,
                                a1.x & b1.x, a1.y & b1.y, a1.z & b1.z, a1.w & b1.w};
         tc_wait_t(tc_smem(&bar_empty[sr_.slot / cpc]), sr_.phase ^ 1, pa_empty);
         // order the stage's TMEM stores after the MMAs that read it (released by the commit)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + a_col + sr_.slot * 64;
+        const long long ts0 = tc_clock();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           if (dbg & 4) break;
@@ -407,7 +417,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        tc_arrive(tc_smem(&bar_full[sr_.slot]));
+        tc_arrive_warp(tc_smem(&bar_full[sr_.slot]), lane);
+        pa_st += tc_clock() - ts0;
       }
       // epilogue: accumulator lane = pair row, columns 0..ncols-1 = items col0..; the groups
       // split the 16-column chunks
@@ -415,7 +426,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long te0 = tc_clock();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t td = tmem + ((uint32_t)(quad * 32) << 16);
-      for (int j0 = 16 * grp; j0 < u.ncols; j0 += 16 * TC_G) {
+      for (int j0 = 16 * grp; j0 < u.ncols; j0 += 16 * TC_GA) {
         uint32_t v[16];
         tc_ld16(td + j0, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      tc_arrive(tc_smem(&bar_dempty));
+      tc_arrive_warp(tc_smem(&bar_dempty), lane);
       pa_epi += tc_clock() - te0;
     }
     if (prof && lane == 0 && warp == 0) {
@@ -437,10 +448,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       atomicAdd((unsigned long long*)&prof[1], (unsigned long long)pa_empty);
       atomicAdd((unsigned long long*)&prof[2], (unsigned long long)pa_dfull);
       atomicAdd((unsigned long long*)&prof[3], (unsigned long long)pa_epi);
+      atomicAdd((unsigned long long*)&prof[13], (unsigned long long)pa_lds);
+      atomicAdd((unsigned long long*)&prof[14], (unsigned long long)pa_st);
     }
-  } else if (warp < 8 * TC_G) {
+  } else if (warp < 4 * (TC_GA + TC_GB)) {
     // ---------------- B producers ----------------
-    const int grp = (warp - 4 * TC_G) >> 2, bt = tid - 32 * 4 * TC_G - TC_B_THREADS * grp;
+    const int grp = (warp - 4 * TC_GA) >> 2, bt = tid - TC_GA * TC_A_THREADS - TC_B_THREADS * grp;
     long long pb_raw = 0, pb_empty = 0;
     TCRing rr_, sr_;
     uint32_t g = 0;
@@ -463,14 +476,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
-        if ((int)(g % TC_G) != grp) continue;
+        if ((int)(g % TC_GB) != grp) continue;
         tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pb_raw);
         const uint8_t* rb = raw + (size_t)rr_.slot * raw_bytes;
         uint4 cur[TC_BT];
 #pragma unroll
         for (int k = 0; k < TC_BT; ++k)
           if (dst[k] != 0xffffffffu) cur[k] = *reinterpret_cast<const uint4*>(rb + roff[k]);
-        tc_arrive(tc_smem(&bar_rempty[rr_.slot]));
+        tc_arrive_warp(tc_smem(&bar_rempty[rr_.slot]), lane);
         tc_wait_t(tc_smem(&bar_empty[sr_.slot / cpc]), sr_.phase ^ 1, pb_empty);
         uint8_t* sp = stages + (size_t)sr_.slot * stage_bytes;
 #pragma unroll
@@ -494,14 +507,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_arrive(tc_smem(&bar_full[sr_.slot]));
+        tc_arrive_warp(tc_smem(&bar_full[sr_.slot]), lane);
       }
     }
     if (prof && bt == 0 && grp == 0) {
       atomicAdd((unsigned long long*)&prof[4], (unsigned long long)pb_raw);
       atomicAdd((unsigned long long*)&prof[5], (unsigned long long)pb_empty);
     }
-  } else if (warp == 8 * TC_G) {
+  } else if (warp == 4 * (TC_GA + TC_GB)) {
     // ---------------- MMA issuer ----------------
     // The whole warp runs the loop (its operands stay warp-uniform, in uniform registers) and
     // one elected lane issues; a single divergent lane would move every operand through
@@ -571,7 +584,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ---------------- bulk-copy loaders (whole warps, elected issue; loader j takes steps g % L == j) --------
-    const int lw = warp - 8 * TC_G - 1;
+    const int lw = warp - 4 * (TC_GA + TC_GB) - 1;
     TCRing rr_;
     uint32_t g = 0;
     long long pl_empty = 0, pl_issue = 0;
