@@ -376,10 +376,16 @@ class FamilyRunner:
         return cpu_rate_queries(self.w, qs, budget, threads, cols_fn=cols_fn)
 
 
-class ItemsetRunner:
-    """cfg4: supports of all 2- and 3-itemsets of the top-200 items (one k_itemsets launch)."""
+# kind::i8 tcgen05.mma throughput measured with tools/microbench6.cu on this pool's B200
+# (A from TMEM, N >= 64): 8190 MAC/clk/SM; MEASURED_PEAKS.json has no int8 figure.
+I8_MAC_PER_CLK_SM = 8190
 
-    kernel = "k_itemsets"
+
+class ItemsetRunner:
+    """cfg4: supports of all 2- and 3-itemsets of the top-200 items (k_pmt_transpose + one
+    k_itemsets_tc launch per column-width class, bracketed by the library's events)."""
+
+    kernel = "k_itemsets_tc"
 
     def __init__(self, args, world, rank, local, torch, ctx):
         from paper_1804_04640_b200 import workloads as W
@@ -411,6 +417,31 @@ class ItemsetRunner:
         self.d2h = 8 * (k * k + self.ntri)
         self.scaling = "weak"
         self.parallelism = "replica" if world == 1 else f"replicas x{world}"
+
+    def roofline(self, k_ms, clocks):
+        """Tensor-bound: useful u8 x u8 MACs = (pairs + triples) x m, as int8 ops (2 per MAC),
+        against the measured kind::i8 MMA rate at the sampled SM clock.  `computed_macs` adds
+        the tiles' padding (rows x 16-column-rounded widths; K4c)."""
+        k, m = len(self.items), self.w.m
+        useful = float(self.npairs + self.ntri) * m
+        rows = [b for b in range(k) for _ in range(b + 1)]  # (b, b) then (a, b) for a < b
+        cols = 0
+        for r0 in range(0, len(rows), 128):
+            c0 = rows[r0] + 1
+            while c0 < k:
+                cols += min(256, (k - c0 + 15) // 16 * 16)
+                c0 += 256
+        computed = 128.0 * cols * ((m + 1023) // 1024 * 1024)
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        peak = 2.0 * I8_MAC_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+        achieved = 2.0 * useful / (k_ms / 1e3) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
+                "frac": achieved / peak, "traffic": load_traffic(self.config), "kernel": self.kernel,
+                "kernel_ms": k_ms, "useful_macs": useful, "computed_macs": computed,
+                "computed_frac": 2.0 * computed / (k_ms / 1e3) / 1e12 / peak,
+                "peak_source": f"measured: tools/microbench6.cu kind::i8 {I8_MAC_PER_CLK_SM} MAC/clk/SM x 148 SMs "
+                               f"x {mhz:.0f} MHz (sampled clock)",
+                "note": "kernel_ms spans k_pmt_transpose + the k_itemsets_tc launches (library events)"}
 
     def step(self):
         self.gdb.itemset_supports(self.items, self.pairs, self.triples)
@@ -547,6 +578,13 @@ def run_ours(args, world, rank, local):
     value = total / (step_ms / 1e3)
     peak, peak_src = load_peaks()
     achieved = r.algo_bytes / (k_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": load_traffic(r.config), "kernel": r.kernel,
+            "kernel_ms": k_ms, "peak_source": peak_src,
+            "note": "achieved = algorithmic bytes per launch / kernel time; frac > 1 means the "
+                    "kernel reuses data from L2/SMEM across queries (reuse regime)"}
+    if hasattr(r, "roofline"):
+        roof = r.roofline(k_ms, clk.summary())
     cfg = r.describe()
     cfg.update({"l2": "flushed (256 MB write) before every timed step", "db_build_seconds": round(r.build_s, 3)})
     line = {
@@ -555,11 +593,7 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded; DESIGN.md Workloads)",
         "config": cfg,
         "scanned_gbs": r.algo_bytes * world / (step_ms / 1e3) / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": load_traffic(r.config), "kernel": r.kernel,
-                     "kernel_ms": k_ms, "peak_source": peak_src,
-                     "note": "achieved = algorithmic bytes per launch / kernel time; frac > 1 means the "
-                             "kernel reuses data from L2/SMEM across queries (reuse regime)"},
+        "roofline": roof,
         "e2e": {"value": total / (e2e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": r.h2d,
                 "d2h_bytes_per_step": r.d2h, "ms_per_step": e2e_step},
         "gpu_launches": launches,

@@ -225,6 +225,20 @@ struct TCRing {
       phase ^= 1;
     }
   }
+  __device__ __forceinline__ void step(uint32_t k, uint32_t n) {  // k <= n
+    slot += k;
+    if (slot >= n) {
+      slot -= n;
+      phase ^= 1;
+    }
+  }
+  __device__ __forceinline__ TCRing plus(uint32_t k, uint32_t n) const {  // any k
+    TCRing r;
+    const uint32_t t = slot + k;
+    r.slot = t % n;
+    r.phase = phase ^ ((t / n) & 1);
+    return r;
+  }
 };
 
 struct TCUnit {
@@ -264,9 +278,9 @@ __device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "TC_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra TC_WAIT;\n\t}" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "r"(0x10000u)  // suspend-time hint (ns): sleep instead of spinning
       : "memory");
 }
 
@@ -378,16 +392,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- A producers (group grp takes steps g % G == grp) + epilogue ----------------
     const int grp = warp >> 2, quad = warp & 3, row = quad * 32 + lane;
     long long pa_raw = 0, pa_empty = 0, pa_dfull = 0, pa_epi = 0, pa_st = 0, pa_lds = 0;
-    TCRing rr_, sr_;
-    uint32_t g = 0;
+    TCRing rr0, sr0;  // ring positions at the start of the current unit
+    uint32_t g = 0;     // CTA step counter at the start of the current unit
     int uc = 0;
     for (int ui = u_begin; ui < u_end; ++ui, ++uc) {
       const TCUnit u = units[ui];
       const int r = u.row0 + row;
       const ISRow rr = r < nrows ? rows[r] : ISRow{-1, -1};
       const TCSlot sl = r < nrows ? slots[r] : TCSlot{0, 0};
-      for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
-        if ((int)(g % ga) != grp) continue;
+      const uint32_t skip = ((uint32_t)grp + ga - g % ga) % ga;  // first own step of the unit
+      TCRing rr_ = rr0.plus(skip, nr), sr_ = sr0.plus(skip, nb);
+      for (int st = u.s0 + (int)skip; st < u.s1; st += ga, rr_.step(ga, nr), sr_.step(ga, nb)) {
         tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pa_raw);
         const long long tq0 = tc_clock();
         const uint8_t* ra = raw + (size_t)rr_.slot * raw_bytes;
@@ -420,6 +435,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_arrive_warp(tc_smem(&bar_full[sr_.slot]), lane);
         pa_st += tc_clock() - ts0;
       }
+      rr0 = rr0.plus(u.s1 - u.s0, nr);
+      sr0 = sr0.plus(u.s1 - u.s0, nb);
+      g += u.s1 - u.s0;
       // epilogue: accumulator lane = pair row, columns 0..ncols-1 = items col0..; the groups
       // split the 16-column chunks
       tc_wait_t(tc_smem(&bar_dfull), uc & 1, pa_dfull);
@@ -455,7 +473,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- B producers ----------------
     const int grp = (warp - 4 * TC_GA) >> 2, bt = tid - TC_GA * TC_A_THREADS - TC_B_THREADS * grp;
     long long pb_raw = 0, pb_empty = 0;
-    TCRing rr_, sr_;
+    TCRing rr0, sr0;
     uint32_t g = 0;
     for (int ui = u_begin; ui < u_end; ++ui) {
       const TCUnit u = units[ui];
@@ -475,8 +493,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           dst[k] = (uint32_t)((il >> 3) * 2048 + (il & 7) * 16);
         }
       }
-      for (int st = u.s0; st < u.s1; ++st, ++g, rr_.next(nr), sr_.next(nb)) {
-        if ((int)(g % TC_GB) != grp) continue;
+      const uint32_t skip = ((uint32_t)grp + TC_GB - g % TC_GB) % TC_GB;
+      TCRing rr_ = rr0.plus(skip, nr), sr_ = sr0.plus(skip, nb);
+      rr0 = rr0.plus(u.s1 - u.s0, nr);
+      sr0 = sr0.plus(u.s1 - u.s0, nb);
+      g += u.s1 - u.s0;
+      for (int st = u.s0 + (int)skip; st < u.s1; st += TC_GB, rr_.step(TC_GB, nr), sr_.step(TC_GB, nb)) {
         tc_wait_t(tc_smem(&bar_rfull[rr_.slot]), rr_.phase, pb_raw);
         const uint8_t* rb = raw + (size_t)rr_.slot * raw_bytes;
         uint4 cur[TC_BT];
@@ -585,7 +607,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------- bulk-copy loaders (whole warps, elected issue; loader j takes steps g % L == j) --------
     const int lw = warp - 4 * (TC_GA + TC_GB) - 1;
-    TCRing rr_;
+    TCRing rr0;
     uint32_t g = 0;
     long long pl_empty = 0, pl_issue = 0;
     const uint32_t raw0 = tc_smem(raw);
@@ -607,8 +629,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       const uint32_t nbb = 32u * (uint32_t)min(ncols, n - col0);
       bytes += nbb;
-      for (int st = s0; st < s1; ++st, ++g, rr_.next(nr)) {
-        if ((int)(g % TC_LOADERS) != lw) continue;
+      const uint32_t skip = ((uint32_t)lw + TC_LOADERS - g % TC_LOADERS) % TC_LOADERS;
+      TCRing rr_ = rr0.plus(skip, nr);
+      rr0 = rr0.plus(s1 - s0, nr);
+      g += s1 - s0;
+      for (int st = s0 + (int)skip; st < s1; st += TC_LOADERS, rr_.step(TC_LOADERS, nr)) {
         tc_wait_t(tc_smem(&bar_rempty[rr_.slot]), rr_.phase ^ 1, pl_empty);
         const long long tl0 = tc_clock();
         const uint32_t bar = tc_smem(&bar_rfull[rr_.slot]);
