@@ -19,6 +19,7 @@
 #include "cs_common.cuh"
 #include "cs_kernels.cuh"
 #include "cs_itemsets.cuh"
+#include "cs_radix.cuh"
 
 using namespace cs;
 
@@ -92,6 +93,12 @@ using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32
 static const HistFn kHist[CS_MAXK][6][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
 #undef CS_HK
+
+// K1r partition kernels per digit count (k >= 2)
+using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
+static const RadixPartFn kRadixPart[CS_MAXK] = {nullptr,         k_radix_part<2>, k_radix_part<3>,
+                                                k_radix_part<4>, k_radix_part<5>, k_radix_part<6>,
+                                                k_radix_part<7>, k_radix_part<8>};
 
 static int hist_path(const QDesc& d) {
   if (d.pack == 4) return P_PACK4;
@@ -188,6 +195,22 @@ struct cs_plan {
   };
   std::vector<SparseQ> sparse;
   std::vector<int32_t> generic_list;  // kind 2 queries
+  // kind 4 (partition class, cs_radix.cuh): queries in wave order, processed in waves whose
+  // partition buffers share one context scratch (slot 23)
+  struct RadixLaunch {
+    int k, first, count;  // k_radix_part<k> over RDescs [first, first + count)
+  };
+  struct RadixWave {
+    std::vector<RadixLaunch> parts;
+    int item0 = 0, nitems = 0;  // k_radix_count items
+  };
+  std::vector<RDesc> rdesc;
+  std::vector<RadixWave> waves;
+  int rx_nchunks = 0;
+  size_t rx_scratch = 0;  // bytes of wave scratch
+  RDesc* d_rdesc = nullptr;
+  RItem* d_ritems = nullptr;
+  int* d_rhead = nullptr;  // one work-queue head per wave
   struct Group {
     int key, first, count;
   };
@@ -267,6 +290,9 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kHist[7][0][0], CS_HIST_THREADS,
                                                         c->hist_smem));
   if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
+  for (RadixPartFn f : kRadixPart)
+    if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
   c->hist_ctas = per_sm * c->num_sms;
@@ -633,6 +659,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_stages = env_int("CS_STAGES", 1) != 0;
   const bool knob_nibble = env_int("CS_NIBBLE", 1) != 0;
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
+  const bool knob_radix = env_int("CS_RADIX", 1) != 0;
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
   for (int q = 0; q < nq; ++q) {
     const int b = var_off[q], e = var_off[q + 1];
@@ -734,6 +761,14 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           d.rlog = rh;
         }
       }
+    } else if (knob_radix && db->nib && k >= 2 && c <= ((int64_t)1 << 24)) {
+      // partition class (cs_radix.cuh): one counting-sort pass by the high bits of the joint
+      // index, then SMEM histograms per 32K-cell group; reads the 4-bit columns
+      d.kind = 4;
+      d.mode = 2;
+      d.nib = 1;
+      d.base = db->nib;
+      for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
     } else if (k >= 2 && c / db->arity[vars[e - 1]] <= smem_words && knob_slice) {
       // slice class: one CTA per value of the most significant digit, C / r_last cells each
       d.kind = 0;
@@ -799,6 +834,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   for (int q = 0; q < nq; ++q) {
     QDesc& d = p->hq[q];
     if (d.kind == 3) {
+      d.nseg = 1;
+      continue;
+    }
+    if (d.kind == 4) {
+      p->score_list.push_back(q);
+      p->needs_global = p->needs_zero = true;
       d.nseg = 1;
       continue;
     }
@@ -933,6 +974,75 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       for (int i : byq[qq]) sorted.push_back(items[i]);
   }
   p->ngitems = (int)sorted.size() - p->nitems;
+  // partition class (kind 4): descriptors in wave order (waves grouped by digit count), count
+  // items per (query, 32K-cell group, chunk range)
+  std::vector<RItem> ritems;
+  {
+    std::vector<int> rq;
+    for (int q = 0; q < nq; ++q)
+      if (p->hq[q].kind == 4) rq.push_back(q);
+    if (!rq.empty()) {
+      std::stable_sort(rq.begin(), rq.end(), [&](int a, int b) { return p->hq[a].k < p->hq[b].k; });
+      const int64_t nchunks = (m + RX_CH - 1) / RX_CH;
+      p->rx_nchunks = (int)nchunks;
+      const size_t buf_b = (size_t)round_up(nchunks * RX_CH * 2, 256);
+      const size_t choff_b = (size_t)round_up(nchunks * (RX_MAX_NB + 1) * 4, 256);
+      const size_t slot = std::max<size_t>(buf_b + choff_b, 256);
+      size_t budget = (size_t)env_int("CS_RADIX_MB", 4096) << 20;
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 2);
+      else cudaGetLastError();
+      const int W = (int)std::max<size_t>(1, std::min<size_t>(budget / slot, rq.size()));
+      p->rx_scratch = slot * (size_t)W;
+      const int64_t cpi = std::max(1, env_int("CS_RADIX_CPI", 2048));
+      const int64_t G = std::max<int64_t>(1, (nchunks + cpi - 1) / cpi);
+      const int64_t cper = std::max<int64_t>(1, (nchunks + G - 1) / G);
+      for (size_t w0 = 0; w0 < rq.size(); w0 += (size_t)W) {
+        cs_plan::RadixWave wave;
+        wave.item0 = (int)ritems.size();
+        for (size_t i = w0; i < std::min(rq.size(), w0 + (size_t)W); ++i) {
+          const int q = rq[i];
+          const QDesc& d = p->hq[q];
+          RDesc r;
+          memset(&r, 0, sizeof r);
+          const size_t s = i - w0;
+          r.buf_off = (int64_t)(s * slot);
+          r.choff_off = (int64_t)(s * slot + buf_b);
+          r.q = q;
+          r.base = d.base;
+          const int64_t C = d.cells;
+          int bb = 10;  // >= 32 buckets where possible (SMEM bucket counters contend less)
+          while (bb < RX_GROUP_BITS && (C >> (bb + 1)) >= 32) ++bb;
+          r.bb = bb;
+          r.nb = (int)((C + (1LL << bb) - 1) >> bb);
+          {
+            uint32_t r8[8];
+            for (int v = 0; v < 8; ++v) r8[v] = v < d.k ? (uint32_t)db->arity[vars[var_off[q] + v]] : 1u;
+            for (int p2 = 0; p2 < 4; ++p2) r.rpair[p2] = r8[2 * p2];
+            r.R0 = r8[0] * r8[1];
+            r.R2 = r8[4] * r8[5];
+            r.P01 = r8[0] * r8[1] * r8[2] * r8[3];
+            for (int v = 0; v < d.k; ++v) r.coff[v] = d.coff[v];
+          }
+          // count sub-group width: ~2 16-B vectors per lane of a chunk's run in one group
+          const double vec = (double)RX_CH * (double)std::min<int64_t>(C, 1LL << RX_GROUP_BITS) / (double)C / 8.0;
+          int wl = 2;
+          while (wl < 5 && (double)(4 << wl) <= vec) ++wl;
+          r.wlog = wl;
+          const int ri = (int)p->rdesc.size();
+          p->rdesc.push_back(r);
+          if (wave.parts.empty() || wave.parts.back().k != d.k) wave.parts.push_back({d.k, ri, 0});
+          wave.parts.back().count++;
+          const int ngrp = (int)((C + (1LL << RX_GROUP_BITS) - 1) >> RX_GROUP_BITS);
+          for (int g = 0; g < ngrp; ++g)
+            for (int64_t c0 = 0; c0 < nchunks; c0 += cper)
+              ritems.push_back(RItem{ri, g, (int32_t)c0, (int32_t)std::min<int64_t>(nchunks, c0 + cper)});
+        }
+        wave.nitems = (int)ritems.size() - wave.item0;
+        p->waves.push_back(wave);
+      }
+    }
+  }
   const double tr2 = trace ? now_ms() : 0.0;
   if (trace)
     fprintf(stderr, "plan_build: classify %.3f ms, items %.3f ms, order %.3f ms\n", tr0 - trc, tr1 - tr0,
@@ -952,7 +1062,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     return o;
   };
   const size_t oq = place(bq), oi = place(bi), os = place(bs), og = place(bg), ov = place(bv),
-               ost = place(bst), oh = place(1024), od = place(sizeof(uint32_t) * std::max(nq, 1));
+               ost = place(bst), oh = place(1024), od = place(sizeof(uint32_t) * std::max(nq, 1)),
+               ord = place(sizeof(RDesc) * std::max<size_t>(p->rdesc.size(), 1)),
+               ori = place(sizeof(RItem) * std::max<size_t>(ritems.size(), 1)),
+               orh = place(sizeof(int) * std::max<size_t>(p->waves.size(), 1));
   char* dblob = nullptr;
   p->transient = transient;
   if (transient) {
@@ -983,7 +1096,11 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   memcpy(hs + og, p->generic_list.data(), sizeof(int32_t) * p->generic_list.size());
   memcpy(hs + ov, gvars.data(), sizeof(int32_t) * gvars.size());
   memcpy(hs + ost, gstride.data(), sizeof(uint32_t) * gstride.size());
+  memcpy(hs + ord, p->rdesc.data(), sizeof(RDesc) * p->rdesc.size());
+  memcpy(hs + ori, ritems.data(), sizeof(RItem) * ritems.size());
   CS_CUDA(cudaMemcpyAsync(dblob, hs, oh, cudaMemcpyHostToDevice, ctx->stream));
+  if (!p->rdesc.empty())
+    CS_CUDA(cudaMemcpyAsync(dblob + ord, hs + ord, orh - ord, cudaMemcpyHostToDevice, ctx->stream));
   p->d_q = (QDesc*)(dblob + oq);
   p->d_items = (WItem*)(dblob + oi);
   p->d_score_list = (int32_t*)(dblob + os);
@@ -992,6 +1109,9 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   p->d_gstride = (uint32_t*)(dblob + ost);
   p->d_head = (int*)(dblob + oh);
   p->d_done = (uint32_t*)(dblob + od);
+  p->d_rdesc = (RDesc*)(dblob + ord);
+  p->d_ritems = (RItem*)(dblob + ori);
+  p->d_rhead = (int*)(dblob + orh);
   if (trace) fprintf(stderr, "plan_build: upload %.3f ms\n", now_ms() - tr2);
   *out = p;
   return CS_OK;
@@ -1298,6 +1418,31 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
                                                   db->cols, db->ld, db->m, dtab);
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
+  }
+  if (!p->waves.empty()) {
+    // partition class: per wave, k_radix_part per digit count, then k_radix_count
+    void* scr = nullptr;
+    CS_TRY(ctx->scratch_get(23, p->rx_scratch, &scr));
+    CS_CUDA(cudaMemsetAsync(p->d_rhead, 0, sizeof(int) * p->waves.size(), ctx->stream));
+    for (size_t w = 0; w < p->waves.size(); ++w) {
+      const auto& wv = p->waves[w];
+      for (const auto& L : wv.parts) {
+        const int total = L.count * p->rx_nchunks;
+        if (total == 0) continue;
+        const int grid = std::min(total, 4 * ctx->num_sms);
+        kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(p->d_rdesc + L.first, L.count,
+                                                                         p->rx_nchunks, db->m, (char*)scr);
+        ctx->launches++;
+        CS_CUDA(cudaGetLastError());
+      }
+      if (wv.nitems > 0 && p->rx_nchunks > 0) {
+        const int grid = std::min(wv.nitems, ctx->num_sms);
+        k_radix_count<<<grid, RC_THREADS, RC_SMEM, ctx->stream>>>(p->d_q, p->d_rdesc, p->d_ritems + wv.item0,
+                                                                  wv.nitems, p->d_rhead + w, dtab, (const char*)scr);
+        ctx->launches++;
+        CS_CUDA(cudaGetLastError());
+      }
+    }
   }
   for (auto& sq : p->sparse) CS_TRY(run_sparse(p, sq, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

@@ -190,6 +190,70 @@ def test_multisegment_and_global_classes(env):
                 os.environ[k] = v
 
 
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _big_table_workload(m, nq=24, seed=7):
+    """cfg5-shaped data (arity U{2..8}) with only tables above SMEM capacity (56K..2^24 cells)."""
+    w = workloads.cfg5(seed=seed, nq=4000, m=m, n=40)
+    qs = [q for q in w.queries if np.prod([int(w.arities[v]) for v in q]) > 60_000][:nq]
+    return w, qs
+
+
+@pytest.mark.parametrize("env", [{}, {"CS_RADIX_CPI": "2", "CS_RADIX_MB": "1"}, {"CS_RADIX": "0"}])
+def test_partition_class_big_tables(env):
+    """Tables above SMEM capacity: the partition class (one counting-sort pass + SMEM group
+    histograms), forced into many count items / one-query waves, and the slice / global
+    classes it replaces (CS_RADIX=0) -- bit-exact tables, LL and nnz vs the radix oracle.
+    m is not a multiple of the 32-row vector or the 16K-row chunk."""
+    def run():
+        c = cs.GpuContext(0)
+        w, qs = _big_table_workload(m=70_001)
+        gdb = w.build_device(c)
+        cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+        u8 = np.vstack([cols[v] for v in range(w.n)])
+        _check_plan_vs_oracle(gdb, u8, w.arities, qs)
+    _with_env(env, run)
+
+
+def test_partition_class_tiny_m(ctx):
+    """Fewer rows than one partition chunk, and a database of 1 row."""
+    for m in (1, 33, 5_000):
+        w, qs = _big_table_workload(m=m, nq=6, seed=9)
+        gdb = w.build_device(ctx)
+        cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+        u8 = np.vstack([cols[v] for v in range(w.n)])
+        _check_plan_vs_oracle(gdb, u8, w.arities, qs)
+
+
+def test_partition_class_mi_and_records(ctx):
+    """Fused MI through the chunked scorer and the record stream of a partition-class table."""
+    w, qs = _big_table_workload(m=40_000, nq=4, seed=13)
+    gdb = w.build_device(ctx)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+    u8 = np.vstack([cols[v] for v in range(w.n)])
+    plan = QueryPlan(gdb, qs)
+    mi = np.zeros(plan.nq)
+    ll = np.zeros(plan.nq)
+    plan.execute(loglik=ll, mi=mi)
+    for i, q in enumerate(qs):
+        recs = O.oracle_records(u8, w.arities, q[0], q[1:])
+        ll1 = O.loglik_of_records(recs)
+        ll0 = O.loglik_of_records(O.oracle_records(u8, w.arities, q[0], ()))
+        assert rel_close(ll[i], ll1, 1e-9)
+        assert abs(mi[i] - O.mi_of_records(recs, w.m)) <= 1e-9 * (abs(ll1) + abs(ll0)) / w.m
+
+
 def test_generic_many_variable_queries(ctx):
     rng = np.random.default_rng(5)
     n, m = 14, 3001
