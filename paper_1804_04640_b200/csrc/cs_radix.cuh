@@ -28,7 +28,8 @@ constexpr int RX_GROUP_BITS = 15;       // cells per count group (128 KB SMEM ta
 constexpr int RX_MAX_NB = 512;          // partition buckets per query (2 per k_radix_part thread)
 constexpr int RX_SMEM = RX_CH * 4 + RX_CH * 2 + (RX_MAX_NB + 1) * 4;  // 4 CTAs per SM
 constexpr int RC_THREADS = 1024;
-constexpr int RC_SMEM = (1 << RX_GROUP_BITS) * 4;
+constexpr int RC_DUMMY = 1 << RX_GROUP_BITS;          // counter for entries outside a run
+constexpr int RC_SMEM = ((1 << RX_GROUP_BITS) + 32) * 4;
 
 // Everything the partition kernels need about one query, precomputed on the host so a CTA
 // reloads it only when its item stream crosses into the next query.
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(head, 1);
-    for (uint32_t i = tid; i < G; i += RC_THREADS) tab[i] = 0u;
+    for (uint32_t i = tid; i < G + 32; i += RC_THREADS) tab[i] = 0u;
     __syncthreads();
     const int it = s_item;
     if (it >= nitems) return;
@@ -279,13 +280,17 @@ __global__ void __launch_bounds__(RC_THREADS, 1)
     const int sub = lane >> wl, sl = lane & (W - 1);
     const char* buf = scratch + r.buf_off;
     const int32_t* choff = reinterpret_cast<const int32_t*>(scratch + r.choff_off);
-    auto bump_masked = [&](const uint4& v, int i0, int s, int e) {
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+    // a vector straddling a run boundary: entries outside [s, e) are redirected to the dummy
+    // counter (short divergent fix-up; the atomics stay convergent)
+    auto clip = [&](uint4& v, int i0, int s, int e) {
+      uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int i = i0 + t;
-        if (i >= s && i < e) atomicAdd(&tab[(wv[t >> 1] >> ((t & 1) * 16)) & 0xffffu], 1u);
+      for (int t = 0; t < 4; ++t) {
+        const int i = i0 + 2 * t;
+        if (i < s || i >= e) wv[t] = (wv[t] & 0xffff0000u) | (uint32_t)RC_DUMMY;
+        if (i + 1 < s || i + 1 >= e) wv[t] = (wv[t] & 0xffffu) | ((uint32_t)RC_DUMMY << 16);
       }
+      v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     };
     auto bump = [&](const uint4& v) {
       const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
@@ -322,8 +327,8 @@ __global__ void __launch_bounds__(RC_THREADS, 1)
         for (int u = 0; u < 4; ++u) {
           const int iu = i + u * step;
           if (iu >= e) break;
-          if (iu >= s && iu + 8 <= e) bump(v[u]);
-          else bump_masked(v[u], iu, s, e);
+          if (iu < s || iu + 8 > e) clip(v[u], iu, s, e);
+          bump(v[u]);
         }
       }
       s = sn;
