@@ -382,10 +382,11 @@ I8_MAC_PER_CLK_SM = 8190
 
 
 class ItemsetRunner:
-    """cfg4: supports of all 2- and 3-itemsets of the top-200 items (k_pmt_transpose + one
-    k_itemsets_tc launch per column-width class, bracketed by the library's events)."""
+    """cfg4: supports of all 2- and 3-itemsets of the top-200 items.  The library picks the
+    class (selector K4d on this sparse data; the tcgen05 bit-GEMM K4c for dense data); the
+    kernel time is bracketed by the library's events around that class's launches."""
 
-    kernel = "k_itemsets_tc"
+    kernel = "k_sel_gram"
 
     def __init__(self, args, world, rank, local, torch, ctx):
         from paper_1804_04640_b200 import workloads as W
@@ -398,6 +399,7 @@ class ItemsetRunner:
         t0 = time.perf_counter()
         self.gdb = w.build_device(ctx)
         sup = self.gdb.count_points([((v,), (1,)) for v in range(w.n)])
+        self.sup = sup
         self.items = W.select_top_items(sup, w.meta["top"])
         self.gdb.bitmap_build(self.items)
         ctx.sync()
@@ -419,6 +421,42 @@ class ItemsetRunner:
         self.parallelism = "replica" if world == 1 else f"replicas x{world}"
 
     def roofline(self, k_ms, clocks):
+        if self.ctx.itemset_class() == "selector":
+            return self.roofline_selector(k_ms, clocks)
+        return self.roofline_tensor(k_ms, clocks)
+
+    def roofline_selector(self, k_ms, clocks):
+        """K4d (rarest-item selection).  HBM roofline over its algorithmic bytes: k_sel_rowmask
+        reads the k state-1 planes and writes the record-major rank masks (wr words per record);
+        k_sel_gram reads each selector's plane and, per record holding the selector of rank r,
+        the ceil(r/32) mask words below r.  Its issue bound is POPC: 2 (r/8)(r/8+1)/2 x 64 / 64
+        popcounts per selected record, reported against 16 POPC/clk/SM (tools/microbench.cu)."""
+        k, m = len(self.items), self.w.m
+        words = -(-(-(-m // 32)) // 32) * 32  # plane words, padded to 32
+        wr = 1 if k <= 32 else 2 if k <= 64 else 4 if k <= 128 else 8
+        supp = sorted((int(self.sup[v]) for v in self.items), reverse=True)
+        gather = sum(s * 4 * ((r + 31) // 32) for r, s in enumerate(supp) if r)
+        algo = 4.0 * words * k + 4.0 * words * 32 * wr + 4.0 * words * (k - 1) + gather
+        popc = 0.0
+        for r, s in enumerate(supp):
+            if r:
+                nb = (r + 7) // 8
+                popc += -(-s // 32) * nb * (nb + 1) / 2 * 64
+        peak, src = load_peaks()
+        achieved = algo / (k_ms / 1e3) / 1e9
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        popc_peak = 16.0 * 148 * mhz * 1e6
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic("cfg4_selector"), "kernel": "k_sel_rowmask+k_sel_gram",
+                "kernel_ms": k_ms, "algorithmic_bytes": algo, "peak_source": src,
+                "popc": {"ops": popc, "achieved_per_s": popc / (k_ms / 1e3), "peak_per_s": popc_peak,
+                         "frac": popc / (k_ms / 1e3) / popc_peak,
+                         "note": "lower bound on issued POPC (batches assumed full)"},
+                "logical_bytes": self.algo_bytes,
+                "note": "selector class (DESIGN.md K4d): every itemset counted under its rarest item over "
+                        "only the records holding it; logical_bytes = the per-itemset plane bytes of survey 8(d)"}
+
+    def roofline_tensor(self, k_ms, clocks):
         """Tensor-bound: useful u8 x u8 MACs = (pairs + triples) x m, as int8 ops (2 per MAC),
         against the measured kind::i8 MMA rate at the sampled SM clock.  `computed_macs` adds
         the tiles' padding (rows x 16-column-rounded widths; K4c)."""
@@ -436,7 +474,7 @@ class ItemsetRunner:
         peak = 2.0 * I8_MAC_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
         achieved = 2.0 * useful / (k_ms / 1e3) / 1e12
         return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
-                "frac": achieved / peak, "traffic": load_traffic(self.config), "kernel": self.kernel,
+                "frac": achieved / peak, "traffic": load_traffic(self.config), "kernel": "k_itemsets_tc",
                 "kernel_ms": k_ms, "useful_macs": useful, "computed_macs": computed,
                 "computed_frac": 2.0 * computed / (k_ms / 1e3) / 1e12 / peak,
                 "peak_source": f"measured: tools/microbench6.cu kind::i8 {I8_MAC_PER_CLK_SM} MAC/clk/SM x 148 SMs "

@@ -47,6 +47,7 @@ extern "C" {
 #define CS_ERR_CUDA (-2)        /* CUDA runtime failure */
 #define CS_ERR_OOM (-3)         /* device allocation failed */
 #define CS_ERR_UNSUPPORTED (-4) /* valid query the engine does not handle (e.g. arity > 256) */
+#define CS_ERR_PARSE (-5)       /* cs_db_load_text: the text is not a valid database (info[] says why) */
 
 /* flags for cs_plan_create / cs_query_batch */
 #define CS_WANT_TABLES 0x1u  /* write dense uint32 N_ijk tables */
@@ -77,6 +78,11 @@ int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches);
  * launches of one cs_plan_execute) or itemset launch; waits for it.  0 if none yet. */
 int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms);
 /* number of SMs / bytes of dynamic smem the histogram kernel uses (diagnostics) */
+/* class that answered the last cs_itemset_supports call on this context (0 = none yet) */
+#define CS_ITEMSETS_BITGEMM 1  /* K4b: Harley-Seal bit-GEMM on the CUDA cores */
+#define CS_ITEMSETS_TENSOR 2   /* K4c: u8 bit-GEMM on tcgen05 tensor cores */
+#define CS_ITEMSETS_SELECTOR 3 /* K4d: rarest-item selection (sparse data) */
+int cs_ctx_itemset_class(cs_ctx* ctx, int32_t* cls);
 int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_bytes, int32_t* hist_ctas);
 
 /* ---- database (reference database.py) ----------------------------------------------- */
@@ -104,6 +110,34 @@ int cs_db_download(cs_db* db, int32_t var, int64_t row0, int64_t nrows, uint8_t*
 /* Total record count of the whole (possibly sharded) database: used for MI's 1/m and
  * MDL's ln m when this handle holds only an instance shard.  Default = own m. */
 int cs_db_set_total_rows(cs_db* db, int64_t m_total);
+/* arities of the n variables (host int32[n]) */
+int cs_db_arities(cs_db* db, int32_t* arities);
+
+/* ---- device-side text ingest (reference load_csv, database.py:160-207) ---------------- */
+/* Parse delimited integer records straight into a device database: line boundaries of
+ * str.splitlines, each line stripped, blank lines dropped, split on `delim` (then each token
+ * stripped) or on whitespace runs, int() base-10 tokens, a file whose smallest state is 1
+ * shifted down by one, arities = observed maxima + 1 unless declared (`arities`, n_arities
+ * entries, checked like Database(data, arities), database.py:36-84).  ASCII grammar: bytes >=
+ * 0x80 are never whitespace or digits.  text: host or device bytes.
+ * delim: a byte, CS_DELIM_SNIFF (',' if the first record holds one, else whitespace; the
+ * reference's default) or CS_DELIM_WHITESPACE.
+ * info (int64[8], always written): [0] CS_LOAD_* status, [1] record width, [2] records,
+ * [3] delimiter used (-1 = whitespace), [4..6] detail (see CS_LOAD_*), [7] 1 if shifted.
+ * Returns CS_ERR_PARSE with info[0] != CS_LOAD_OK when the reference would raise
+ * DatabaseLoadError; CS_ERR_UNSUPPORTED for states above 255. */
+#define CS_DELIM_SNIFF (-1)
+#define CS_DELIM_WHITESPACE (-2)
+#define CS_LOAD_OK 0
+#define CS_LOAD_NO_RECORDS 1  /* "no records found" */
+#define CS_LOAD_BAD_RECORD 2  /* info[4] = first bad record (ragged or non-integer token);
+                               * its stripped line is text[info[5] .. info[6]) */
+#define CS_LOAD_NEGATIVE 3    /* info[4] = smallest state */
+#define CS_LOAD_ARITY_COUNT 4 /* info[4] = number of declared arities */
+#define CS_LOAD_ARITY_SHORT 5 /* info[4] = row, [5] = variable, [6] = state */
+#define CS_LOAD_ARITY_ZERO 6  /* a declared arity < 1 */
+int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, int32_t delim,
+                    const int32_t* arities, int32_t n_arities, cs_db** out, int64_t* info);
 
 /* ---- bitmap index (reference bitmap.py:29-66) ---------------------------------------- */
 /* Replaces build_bitmap_index (bitmap.py:53-66): one bit plane per (variable, state),

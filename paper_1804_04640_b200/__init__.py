@@ -43,6 +43,7 @@ from .harness import (
     Strategy,
     bench_random,
     learn_parents,
+    load_csv_device,
     make_strategies,
     mine_rules,
     shared_context,
@@ -85,6 +86,7 @@ __all__ = [
     "Strategy",
     "bench_random",
     "learn_parents",
+    "load_csv_device",
     "make_strategies",
     "mine_rules",
     "shared_context",

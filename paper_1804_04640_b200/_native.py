@@ -20,6 +20,12 @@ CS_ERR_INVALID = -1
 CS_ERR_CUDA = -2
 CS_ERR_OOM = -3
 CS_ERR_UNSUPPORTED = -4
+CS_ERR_PARSE = -5
+
+CS_DELIM_SNIFF = -1
+CS_DELIM_WHITESPACE = -2
+CS_LOAD_OK, CS_LOAD_NO_RECORDS, CS_LOAD_BAD_RECORD, CS_LOAD_NEGATIVE = 0, 1, 2, 3
+CS_LOAD_ARITY_COUNT, CS_LOAD_ARITY_SHORT, CS_LOAD_ARITY_ZERO = 4, 5, 6
 
 CS_WANT_TABLES = 0x1
 CS_WANT_LOGLIK = 0x2
@@ -40,6 +46,7 @@ SIGNATURES = [
     ("cs_ctx_sync", c_int, [_P]),
     ("cs_ctx_launch_count", c_int, [_P, POINTER(c_int64)]),
     ("cs_ctx_last_kernel_ms", c_int, [_P, POINTER(ctypes.c_float)]),
+    ("cs_ctx_itemset_class", c_int, [_P, POINTER(c_int32)]),
     ("cs_ctx_info", c_int, [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
     ("cs_db_create", c_int, [_P, _P, c_int32, c_int64, c_int64, _P, POINTER(_P)]),
     ("cs_db_create_empty", c_int, [_P, c_int32, c_int64, _P, POINTER(_P)]),
@@ -49,6 +56,8 @@ SIGNATURES = [
     ("cs_db_columns", c_int, [_P, POINTER(_P), POINTER(c_int64)]),
     ("cs_db_download", c_int, [_P, c_int32, c_int64, c_int64, _P]),
     ("cs_db_set_total_rows", c_int, [_P, c_int64]),
+    ("cs_db_arities", c_int, [_P, _P]),
+    ("cs_db_load_text", c_int, [_P, _P, c_int64, c_int32, _P, c_int32, POINTER(_P), _P]),
     ("cs_bitmap_build", c_int, [_P, c_int32, _P]),
     ("cs_bitmap_plane", c_int, [_P, c_int32, c_int32, POINTER(_P), POINTER(c_int64)]),
     ("cs_plan_create", c_int, [_P, c_int32, _P, _P, c_uint32, POINTER(_P)]),
@@ -101,7 +110,15 @@ def check(rc: int) -> None:
         from .database import InvalidQueryError
 
         raise InvalidQueryError(msg)
+    if rc == CS_ERR_UNSUPPORTED:
+        from .database import UnsupportedQueryError
+
+        raise UnsupportedQueryError(msg)
     raise EngineError(rc, msg)
+
+
+def last_error() -> str:
+    return (lib.cs_last_error() or b"").decode(errors="replace")
 
 
 def ptr(x) -> int | None:

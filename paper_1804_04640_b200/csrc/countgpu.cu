@@ -13,6 +13,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/countstream_gpu.h"
@@ -20,6 +21,8 @@
 #include "cs_kernels.cuh"
 #include "cs_itemsets.cuh"
 #include "cs_radix.cuh"
+#include "cs_ingest.cuh"
+#include "cs_itemsets_sel.cuh"
 
 using namespace cs;
 
@@ -122,6 +125,7 @@ struct cs_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the last K1 launch
   bool ev_valid = false;
   int64_t launches = 0;
+  int32_t itemset_class = 0;  // class of the last cs_itemset_supports call (CS_ITEMSETS_*)
   // grow-only device scratch for host-bound outputs
   std::map<int, std::pair<void*, size_t>> scratch;
   // grow-only pinned staging
@@ -351,6 +355,12 @@ extern "C" int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms) {
   return CS_OK;
 }
 
+extern "C" int cs_ctx_itemset_class(cs_ctx* ctx, int32_t* cls) {
+  if (!ctx || !cls) return fail(CS_ERR_INVALID, "cs_ctx_itemset_class: NULL argument");
+  *cls = ctx->itemset_class;
+  return CS_OK;
+}
+
 extern "C" int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_bytes,
                            int32_t* hist_ctas) {
   if (!ctx) return fail(CS_ERR_INVALID, "cs_ctx_info: NULL ctx");
@@ -558,9 +568,349 @@ extern "C" int cs_db_download(cs_db* db, int32_t var, int64_t row0, int64_t nrow
   return CS_OK;
 }
 
+extern "C" int cs_db_arities(cs_db* db, int32_t* arities) {
+  if (!db || !arities) return fail(CS_ERR_INVALID, "cs_db_arities: NULL argument");
+  std::copy(db->arity.begin(), db->arity.end(), arities);
+  return CS_OK;
+}
+
 extern "C" int cs_db_set_total_rows(cs_db* db, int64_t m_total) {
   if (!db || m_total < db->m) return fail(CS_ERR_INVALID, "cs_db_set_total_rows: bad argument");
   db->m_total = m_total;
+  return CS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// text ingest (cs_ingest.cuh; reference load_csv, database.py:160-207)
+
+namespace {
+
+// RAII bag of stream-ordered temporaries
+struct TmpBag {
+  cudaStream_t st;
+  std::vector<void*> p;
+  explicit TmpBag(cudaStream_t s) : st(s) {}
+  ~TmpBag() {
+    for (void* x : p) cudaFreeAsync(x, st);
+  }
+  template <class T>
+  int get(size_t count, T** out) {
+    void* x = nullptr;
+    cudaError_t e = cudaMallocAsync(&x, std::max<size_t>(count * sizeof(T), 16), st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(e == cudaErrorMemoryAllocation ? CS_ERR_OOM : CS_ERR_CUDA, "ingest scratch (%zu B): %s",
+                  count * sizeof(T), cudaGetErrorString(e));
+    }
+    p.push_back(x);
+    *out = static_cast<T*>(x);
+    return CS_OK;
+  }
+};
+
+// exclusive scan of n int64 on the context stream (tiles of TX_SCAN_TILE, recursive on totals)
+int scan64(cs_ctx* ctx, TmpBag& bag, int64_t* d, int64_t n) {
+  const int64_t tiles = (n + TX_SCAN_TILE - 1) / TX_SCAN_TILE;
+  if (tiles <= 1) {
+    k_scan64_tiles<<<1, 1024, 0, ctx->stream>>>(d, n, nullptr);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+    return CS_OK;
+  }
+  int64_t* sums = nullptr;
+  CS_TRY(bag.get(tiles, &sums));
+  k_scan64_tiles<<<(unsigned)tiles, 1024, 0, ctx->stream>>>(d, n, sums);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_TRY(scan64(ctx, bag, sums, tiles));
+  k_scan64_add<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(d, n, sums);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
+template <class T>
+int d2h(cs_ctx* ctx, T* host, const T* dev, size_t count = 1) {
+  CS_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+// host -> device copy of a large pageable buffer: pinned in place when the driver allows it,
+// else staged through the context's pinned buffer (two halves, event-guarded)
+int h2d_large(cs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+    CS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));  // pinned: DMA directly
+    return CS_OK;
+  }
+  cudaGetLastError();
+  if (bytes >= (1u << 30) &&
+      cudaHostRegister(const_cast<void*>(src), bytes, cudaHostRegisterReadOnly) == cudaSuccess) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    cudaError_t e2 = cudaStreamSynchronize(ctx->stream);
+    cudaHostUnregister(const_cast<void*>(src));
+    CS_CUDA(e);
+    CS_CUDA(e2);
+    return CS_OK;
+  }
+  cudaGetLastError();
+  const size_t CH = 32u << 20;
+  void* pin = nullptr;
+  CS_TRY(ctx->pinned_get(2 * CH, &pin));
+  cudaEvent_t ev[2];
+  CS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  int rc = CS_OK;
+  for (size_t off = 0, i = 0; off < bytes && rc == CS_OK; off += CH, ++i) {
+    const size_t len = std::min(CH, bytes - off);
+    char* stage = static_cast<char*>(pin) + (i & 1) * CH;
+    if (i >= 2 && cudaEventSynchronize(ev[i & 1]) != cudaSuccess) rc = fail(CS_ERR_CUDA, "h2d stage wait");
+    if (rc != CS_OK) break;
+    // pageable -> pinned with several host threads (one memcpy thread moves ~10 GB/s)
+    const char* from = static_cast<const char*>(src) + off;
+    const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, len >> 22));
+    std::vector<std::thread> pool;
+    const size_t per = (len + nt - 1) / nt;
+    for (int t = 1; t < nt; ++t) {
+      const size_t a = t * per, b = std::min(len, a + per);
+      if (a < b) pool.emplace_back([=] { memcpy(stage + a, from + a, b - a); });
+    }
+    memcpy(stage, from, std::min(len, per));
+    for (auto& th : pool) th.join();
+    if (cudaMemcpyAsync(static_cast<char*>(dst) + off, stage, len, cudaMemcpyHostToDevice, ctx->stream) !=
+            cudaSuccess ||
+        cudaEventRecord(ev[i & 1], ctx->stream) != cudaSuccess)
+      rc = fail(CS_ERR_CUDA, "h2d staged copy failed");
+  }
+  cudaStreamSynchronize(ctx->stream);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, int32_t delim,
+                               const int32_t* arities, int32_t n_arities, cs_db** out, int64_t* info) {
+  if (!ctx || !out || !info || (!text && nbytes > 0) || nbytes < 0)
+    return fail(CS_ERR_INVALID, "cs_db_load_text: bad argument");
+  if (delim < CS_DELIM_WHITESPACE || delim > 255)
+    return fail(CS_ERR_INVALID, "cs_db_load_text: delimiter must be a byte, CS_DELIM_SNIFF or CS_DELIM_WHITESPACE");
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  *out = nullptr;
+  if (nbytes == 0) {
+    info[0] = CS_LOAD_NO_RECORDS;
+    return fail(CS_ERR_PARSE, "no records found");
+  }
+  CS_CUDA(cudaSetDevice(ctx->device));
+  static bool attrs = false;
+  if (!attrs) {
+    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    attrs = true;
+  }
+  cudaStream_t st = ctx->stream;
+  static bool pool_kept = false;
+  if (!pool_kept) {  // keep freed scratch in the stream-ordered pool between loads
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_kept = true;
+  }
+  TmpBag bag(st);
+  // 1. text on the device, zero padded (vector loads and the look-ahead byte stay in bounds)
+  const int64_t tbytes = round_up(nbytes, 64) + TX_PAD;
+  uint8_t* dt = nullptr;
+  CS_TRY(bag.get(tbytes, &dt));
+  CS_CUDA(cudaMemsetAsync(dt + nbytes, 0, tbytes - nbytes, st));
+  if (is_device_ptr(text)) {
+    CS_CUDA(cudaMemcpyAsync(dt, text, nbytes, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CS_TRY(h2d_large(ctx, dt, text, nbytes));
+  }
+  // 2. line boundaries
+  const int64_t nch = (nbytes + TX_CHUNK - 1) / TX_CHUNK;
+  if (nch > INT32_MAX) return fail(CS_ERR_UNSUPPORTED, "text too large");
+  int64_t* cnt = nullptr;
+  CS_TRY(bag.get(nch + 1, &cnt));
+  CS_CUDA(cudaMemsetAsync(cnt + nch, 0, sizeof(int64_t), st));
+  k_txt_breaks<false><<<(unsigned)nch, TX_THREADS, 0, st>>>(dt, nbytes, cnt, nullptr, nullptr);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_TRY(scan64(ctx, bag, cnt, nch + 1));
+  int64_t nbrk = 0;
+  CS_TRY(d2h(ctx, &nbrk, cnt + nch));
+  int64_t* brk = nullptr;
+  CS_TRY(bag.get(nbrk + 1, &brk));
+  k_txt_breaks<true><<<(unsigned)nch, TX_THREADS, 0, st>>>(dt, nbytes, nullptr, cnt, brk);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  // 3. lines -> stripped bounds, non-empty flags -> record map
+  const int64_t nl = nbrk + 1;
+  int64_t *la = nullptr, *lb = nullptr, *ne = nullptr, *rank = nullptr;
+  CS_TRY(bag.get(nl, &la));
+  CS_TRY(bag.get(nl, &lb));
+  CS_TRY(bag.get(nl + 1, &ne));
+  CS_TRY(bag.get(nl + 1, &rank));
+  const unsigned lgrid = (unsigned)std::min<int64_t>((nl + 7) / 8, (int64_t)ctx->num_sms * 16);
+  k_txt_lines<<<lgrid, 256, 0, st>>>(dt, nbytes, brk, nl, la, lb, ne);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_CUDA(cudaMemsetAsync(ne + nl, 0, sizeof(int64_t), st));
+  CS_CUDA(cudaMemcpyAsync(rank, ne, sizeof(int64_t) * (nl + 1), cudaMemcpyDeviceToDevice, st));
+  CS_TRY(scan64(ctx, bag, rank, nl + 1));
+  int64_t nrec = 0;
+  CS_TRY(d2h(ctx, &nrec, rank + nl));
+  if (nrec == 0) {
+    info[0] = CS_LOAD_NO_RECORDS;
+    return fail(CS_ERR_PARSE, "no records found");
+  }
+  if (nrec > INT32_MAX) return fail(CS_ERR_UNSUPPORTED, "more than 2^31-1 records");
+  int64_t* rec_line = nullptr;
+  CS_TRY(bag.get(nrec, &rec_line));
+  k_txt_compact<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(ne, rank, nl, rec_line);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  // 4. delimiter sniff and record width from the first record (reference: `"," in lines[0]`)
+  int64_t* dhead = nullptr;
+  CS_TRY(bag.get(4, &dhead));
+  k_txt_head<<<1, 32, 0, st>>>(dt, la, lb, rec_line, delim >= 0 ? delim : ',', dhead);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  int64_t head[4];
+  CS_TRY(d2h(ctx, head, dhead, 4));
+  int32_t kd = delim;  // kernel delimiter: < 0 = whitespace
+  if (delim == CS_DELIM_SNIFF) kd = head[0] ? ',' : -1;
+  if (kd == CS_DELIM_WHITESPACE) kd = -1;
+  const int64_t width = kd < 0 ? head[1] : head[2];
+  info[1] = width;
+  info[2] = nrec;
+  info[3] = kd;
+  if (width > 50000) return fail(CS_ERR_UNSUPPORTED, "records of %lld values: the loader supports <= 50000", (long long)width);
+  // 5. database with placeholder arities (fixed below), then the parse
+  std::vector<int32_t> ones(width, 1);
+  cs_db* db = nullptr;
+  CS_TRY(db_alloc(ctx, (int32_t)width, nrec, ones.data(), &db));
+  int rc = CS_OK;
+  auto drop = [&](int code) {
+    cs_db_destroy(db);
+    return code;
+  };
+  int *colmax = nullptr, *gmin = nullptr;
+  unsigned long long* bad = nullptr;
+  if ((rc = bag.get(width, &colmax)) || (rc = bag.get(1, &gmin)) || (rc = bag.get(1, &bad))) return drop(rc);
+  cudaMemsetAsync(colmax, 0x80, sizeof(int) * width, st);  // 0x80808080 < -TX_SAT
+  cudaMemsetAsync(gmin, 0x7f, sizeof(int), st);            // 0x7f7f7f7f > TX_SAT
+  cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st);
+  int tr = 256;
+  while (tr > 32 && 4 * width + width * (int64_t)tr > 48 * 1024) tr >>= 1;
+  const bool direct = 4 * width + width * (int64_t)tr > 200 * 1024;
+  // text staging: the tile's span (~tr records of nbytes/nrec bytes), 16-B rounded, <= 64 KB
+  const double avg = (double)nbytes / (double)nrec;
+  const int64_t tile_b = direct ? 0 : round_up(width * (int64_t)tr, 16);
+  const int32_t stage = (int32_t)std::max<int64_t>(
+      0, std::min<int64_t>(round_up((int64_t)(avg * tr * 1.25) + 64, 16), 200 * 1024 - 4 * width - tile_b));
+  const size_t smem = 4 * width + tile_b + stage;
+  const unsigned pgrid = (unsigned)((nrec + tr - 1) / tr);
+  if (direct)
+    k_txt_parse<true><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
+                                                       db->cols, db->ld, colmax, gmin, bad, stage);
+  else
+    k_txt_parse<false><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
+                                                        db->cols, db->ld, colmax, gmin, bad, stage);
+  ctx->launches++;
+  if (cudaGetLastError() != cudaSuccess) return drop(fail(CS_ERR_CUDA, "k_txt_parse launch failed"));
+  unsigned long long hbad = 0;
+  int hmin = 0;
+  std::vector<int> cmax(width);
+  if ((rc = d2h(ctx, &hbad, bad)) || (rc = d2h(ctx, &hmin, gmin)) || (rc = d2h(ctx, cmax.data(), colmax, width)))
+    return drop(rc);
+  // 6. the reference's error order: first bad record, negative states, then Database checks
+  if (hbad != ~0ull) {
+    int64_t ln = 0;
+    if ((rc = d2h(ctx, &ln, rec_line + hbad)) || (rc = d2h(ctx, &info[5], la + ln)) || (rc = d2h(ctx, &info[6], lb + ln)))
+      return drop(rc);
+    info[0] = CS_LOAD_BAD_RECORD;
+    info[4] = (int64_t)hbad;
+    return drop(fail(CS_ERR_PARSE, "record %llu is ragged or holds a non-integer token", hbad));
+  }
+  if (hmin < 0) {
+    info[0] = CS_LOAD_NEGATIVE;
+    info[4] = hmin;
+    return drop(fail(CS_ERR_PARSE, "negative state %d; states must be >= 0", hmin));
+  }
+  const bool shift = hmin == 1;
+  if (shift) {
+    dim3 g((unsigned)std::min<int64_t>((nrec / 4 + 255) / 256 + 1, 1024), (unsigned)width);
+    k_txt_shift<<<g, 256, 0, st>>>(db->cols, db->ld, nrec);
+    ctx->launches++;
+    if (cudaGetLastError() != cudaSuccess) return drop(fail(CS_ERR_CUDA, "k_txt_shift launch failed"));
+  }
+  info[7] = shift;
+  std::vector<int32_t> ar(width);
+  for (int64_t i = 0; i < width; ++i) ar[i] = cmax[i] - (shift ? 1 : 0) + 1;  // observed arity
+  // states above 255 do not fit the uint8 layout (Database.columns_u8's check, raised before the
+  // declared-arity checks because the stored bytes no longer hold them)
+  const int32_t amax = *std::max_element(ar.begin(), ar.end());
+  if (amax > CS_MAX_ARITY)
+    return drop(fail(CS_ERR_UNSUPPORTED,
+                     "the GPU engine stores states as uint8; arities above 256 are unsupported (max arity %d)",
+                     amax));
+  if (arities) {
+    if (n_arities != width) {
+      info[0] = CS_LOAD_ARITY_COUNT;
+      info[4] = n_arities;
+      return drop(fail(CS_ERR_PARSE, "expected %lld arities, got %d", (long long)width, n_arities));
+    }
+    for (int64_t i = 0; i < width; ++i) {
+      if (arities[i] < ar[i]) {  // first short variable, then its first offending row
+        const int32_t ai = std::max(0, arities[i]);
+        unsigned long long* dbad = nullptr;
+        if ((rc = bag.get(1, &dbad))) return drop(rc);
+        cudaMemcpyAsync(db->d_arity + i, &ai, sizeof(int32_t), cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st);
+        dim3 g((unsigned)std::min<int64_t>((nrec + 255) / 256, 1024), 1);
+        k_check_states<<<g, 256, 0, st>>>(db->cols + i * db->ld, db->ld, nrec, db->d_arity + i, dbad);
+        ctx->launches++;
+        unsigned long long row = 0;
+        uint8_t state = 0;
+        if ((rc = d2h(ctx, &row, dbad)) || (rc = d2h(ctx, &state, db->cols + i * db->ld + row))) return drop(rc);
+        info[0] = CS_LOAD_ARITY_SHORT;
+        info[4] = (int64_t)row;
+        info[5] = i;
+        info[6] = state;
+        return drop(fail(CS_ERR_PARSE, "row %llu: variable %lld has state %d, exceeding declared arity %d",
+                         row + 1, (long long)i, (int)state, arities[i]));
+      }
+    }
+    for (int64_t i = 0; i < width; ++i) ar[i] = arities[i];
+    for (int64_t i = 0; i < width; ++i)
+      if (ar[i] < 1) {
+        info[0] = CS_LOAD_ARITY_ZERO;
+        return drop(fail(CS_ERR_PARSE, "every arity must be at least 1"));
+      }
+    if (*std::max_element(ar.begin(), ar.end()) > CS_MAX_ARITY)
+      return drop(fail(CS_ERR_UNSUPPORTED,
+                       "the GPU engine stores states as uint8; arities above 256 are unsupported (max arity %d)",
+                       *std::max_element(ar.begin(), ar.end())));
+  }
+  db->arity = ar;
+  CS_CUDA(cudaMemcpyAsync(db->d_arity, ar.data(), sizeof(int32_t) * width, cudaMemcpyHostToDevice, st));
+  if (db->nib && *std::max_element(ar.begin(), ar.end()) > 16) {
+    CS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(db->nib);
+    db->nib = nullptr;
+    db->ldn = 0;
+  }
+  if ((rc = db_pack(db, 0, db->n))) return drop(rc);
+  CS_CUDA(cudaStreamSynchronize(st));
+  *out = db;
   return CS_OK;
 }
 
@@ -1650,6 +2000,128 @@ extern "C" int cs_count_points(cs_db* db, int32_t nq, const int32_t* var_off, co
   return CS_OK;
 }
 
+// K4d (cs_itemsets_sel.cuh): supports by rarest-item selection.  Returns 1 (declined, nothing
+// written) when the cost model prefers the dense bit-GEMM for this data, CS_OK when done.
+static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*>& hp, int64_t* pairs,
+                             int64_t* triples, int mode) {
+  cs_ctx* ctx = db->ctx;
+  const int64_t W = db->words;  // multiple of 32 words
+  const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
+  // 1. item supports
+  const size_t bp = sizeof(void*) * n;
+  size_t off = 0;
+  auto place = [&](size_t b) {
+    size_t o = off;
+    off = round_up(off + b, 256);
+    return o;
+  };
+  const size_t op = place(bp), ors = place(bp), osu = place(sizeof(unsigned long long) * n),
+               ori = place(sizeof(int16_t) * SEL_MAXN), ohd = place(sizeof(int));
+  const size_t meta_end = off;
+  void* blob = nullptr;
+  CS_TRY(ctx->scratch_get(11, off, &blob));
+  char* d = (char*)blob;
+  CS_CUDA(cudaMemcpyAsync(d + op, hp.data(), bp, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d + osu, 0, sizeof(unsigned long long) * n, ctx->stream));
+  k_sel_support<<<dim3(8, n), 256, 0, ctx->stream>>>((const uint32_t* const*)(d + op), W,
+                                                     (unsigned long long*)(d + osu));
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> supp(n);
+  CS_CUDA(cudaMemcpyAsync(supp.data(), d + osu, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  // 2. ranks (support descending, ties by position) and the cost model
+  std::vector<int> rank_item(n);
+  std::iota(rank_item.begin(), rank_item.end(), 0);
+  std::stable_sort(rank_item.begin(), rank_item.end(), [&](int a, int b) { return supp[a] > supp[b]; });
+  const double m = (double)db->m;
+  // cost model: k_sel_gram issues (r/8)^2 x 2 popcounts per selected record of rank r (8 x 8
+  // register blocks over 32-record batches), plus the record gathers
+  std::vector<double> cost(n, 0.0);
+  double total = 0.0, gathered = 0.0;
+  for (int r = 1; r < n; ++r) {
+    const double sr = (double)supp[rank_item[r]];
+    const double nb = (r + 7) / 8;
+    cost[r] = sr * (nb * (nb + 1) + 4.0) + (double)W / 16.0;
+    total += cost[r];
+    gathered += sr;
+  }
+  // measured rates (B200): POPC ~16/clk/SM at ~60% issue; the tcgen05 bit-GEMM ~7e14 MAC/s
+  const double sparse_s = total / (ctx->num_sms * 16.0 * 1.9e9 * 0.6) + gathered * 32.0 / 3e12 +
+                          (double)W * 32 * 32 / 5e12;
+  const double dense_s = ((double)ntri + 0.5 * n * (n - 1)) * m / 7e14;
+  if (mode < 0 && sparse_s > dense_s) return 1;
+  // 3. record-major rank masks
+  const int wr = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
+  // units: (rank, word range) with ~equal cost, ranges in multiples of 512 words (16 warps x 32)
+  const double target = std::max(1.0, total / (ctx->num_sms * 8.0));
+  std::vector<SelUnit> units;
+  std::vector<double> ucost;
+  for (int r = 1; r < n; ++r) {
+    if (!cost[r]) continue;
+    int64_t chunks = std::max<int64_t>(1, (int64_t)std::ceil(cost[r] / target));
+    const int64_t per = round_up((W + chunks - 1) / chunks, 512);
+    for (int64_t w0 = 0; w0 < W; w0 += per) {
+      units.push_back(SelUnit{r, 0, w0, std::min(W, w0 + per)});
+      ucost.push_back(cost[r] * (double)(std::min(W, w0 + per) - w0) / (double)W + 64.0 * r);
+    }
+  }
+  std::vector<int> order(units.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ucost[a] > ucost[b]; });
+  std::vector<SelUnit> sorted(units.size());
+  for (size_t i = 0; i < order.size(); ++i) sorted[i] = units[order[i]];
+  const size_t bu = sizeof(SelUnit) * std::max<size_t>(1, sorted.size());
+  const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
+  const size_t brm = sizeof(uint32_t) * (size_t)W * 32 * wr;
+  const size_t ou = place(bu), opr = place(bpairs), otr = place(btri), orm = place(brm);
+  CS_TRY(ctx->scratch_get(11, off, &blob));  // grow (the support pass above is complete)
+  d = (char*)blob;
+  std::vector<const uint32_t*> rp(n);
+  std::vector<int16_t> ri(SEL_MAXN, 0);
+  for (int r = 0; r < n; ++r) rp[r] = hp[rank_item[r]], ri[r] = (int16_t)rank_item[r];
+  void* hst = nullptr;
+  const size_t hbytes = meta_end + bu;
+  CS_TRY(ctx->pinned_get(hbytes, &hst));
+  char* h = (char*)hst;
+  memcpy(h + op, hp.data(), bp);
+  memcpy(h + ors, rp.data(), bp);
+  memcpy(h + ori, ri.data(), sizeof(int16_t) * SEL_MAXN);
+  if (!sorted.empty()) memcpy(h + ou, sorted.data(), sizeof(SelUnit) * sorted.size());
+  CS_CUDA(cudaMemcpyAsync(d, h, ohd, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemcpyAsync(d + ou, h + ou, bu, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d + ohd, 0, sizeof(int), ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d + opr, 0, otr - opr + btri, ctx->stream));
+  const int Rw = (int)round_up(n - 1, 8);  // Y row stride (ranks < rmax = n - 1)
+  const size_t smem = sizeof(uint32_t) * (SEL_LCAP + (size_t)SEL_MAXB * Rw);
+  static bool attr = false;
+  if (!attr) {
+    CS_CUDA(cudaFuncSetAttribute((const void*)k_sel_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  ctx->itemset_class = CS_ITEMSETS_SELECTOR;
+  CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+  k_sel_rowmask<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((const uint32_t* const*)(d + ors), n, W, wr,
+                                                          (uint32_t*)(d + orm));
+  ctx->launches++;
+  if (!sorted.empty()) {
+    k_sel_gram<<<ctx->num_sms, SEL_THREADS, smem, ctx->stream>>>(
+        (const uint32_t* const*)(d + ors), (const uint32_t*)(d + orm), wr, (const int16_t*)(d + ori), n,
+        (const SelUnit*)(d + ou), (int)sorted.size(), (int*)(d + ohd), Rw, (unsigned long long*)(d + opr),
+        (unsigned long long*)(d + otr));
+    ctx->launches++;
+  }
+  CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->ev_valid = true;
+  CS_CUDA(cudaGetLastError());
+  const cudaMemcpyKind kp = is_device_ptr(pairs) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const cudaMemcpyKind kt = is_device_ptr(triples) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (pairs) CS_CUDA(cudaMemcpyAsync(pairs, d + opr, bpairs, kp, ctx->stream));
+  if (triples && ntri) CS_CUDA(cudaMemcpyAsync(triples, d + otr, sizeof(uint64_t) * ntri, kt, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
 extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* items, int64_t* pairs,
                                    int64_t* triples) {
   if (!db) return fail(CS_ERR_INVALID, "cs_itemset_supports: NULL db");
@@ -1679,6 +2151,12 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
   const int64_t W = db->words;  // multiple of 32 words
   const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
   const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
+  // sparse data: count every itemset under its rarest item (K4d) when the cost model says so
+  const int sel_mode = env_int("CS_ITEMSETS_SEL", -1);  // -1 auto, 0 never, 1 always (read per call)
+  if (sel_mode != 0 && n <= SEL_MAXN && n >= 2) {
+    const int rc = itemsets_selector(db, n, hp, pairs, triples, sel_mode);
+    if (rc != 1) return rc;
+  }
   static const int use_tc = env_int("CS_ITEMSETS_TC", 1);
   if (use_tc) {
     // tensor-core path (K4c, cs_itemsets.cuh).  Tiles = (128-row block, <= 256-column chunk
@@ -1883,6 +2361,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     CS_CUDA(cudaMemcpyAsync(d, h, meta, cudaMemcpyHostToDevice, ctx->stream));
     CS_CUDA(cudaMemsetAsync(d + opr, 0, otr - opr + btri, ctx->stream));
     if (tc_prof) CS_CUDA(cudaMemsetAsync(d + opf, 0, 1024, ctx->stream));
+    ctx->itemset_class = CS_ITEMSETS_TENSOR;
     CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     k_pmt_transpose<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((const uint32_t* const*)(d + op), n, nsteps,
                                                               (uint4*)(d + opm));
@@ -1929,6 +2408,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     }
     return CS_OK;
   }
+  ctx->itemset_class = CS_ITEMSETS_BITGEMM;
   std::vector<std::pair<int, int>> tiles;
   for (int r0 = 0; r0 < nrows; r0 += IS_ROWS) {
     const int minb = rows[r0].b;

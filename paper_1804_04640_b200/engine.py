@@ -30,6 +30,39 @@ def encode_queries(queries: Iterable[Sequence[int]]) -> tuple[np.ndarray, np.nda
     return off, flat
 
 
+def _load_message(source: str, buf, info: np.ndarray, arities) -> str:
+    """The reference's DatabaseLoadError text (database.py:184-207, :53-77) for a
+    cs_db_load_text failure; only the one offending line is read back on the host."""
+    kind = int(info[0])
+    if kind == N.CS_LOAD_NO_RECORDS:
+        return f"{source}: no records found"
+    if kind == N.CS_LOAD_NEGATIVE:
+        return f"{source}: negative state {int(info[4])}; states must be >= 0"
+    if kind == N.CS_LOAD_ARITY_COUNT:
+        return f"expected {int(info[1])} arities, got {(int(info[4]),)}"
+    if kind == N.CS_LOAD_ARITY_SHORT:
+        var = int(info[5])
+        return (f"row {int(info[4]) + 1}: variable {var} has state {int(info[6])}, "
+                f"exceeding declared arity {int(arities[var])}")
+    if kind == N.CS_LOAD_ARITY_ZERO:
+        return "every arity must be at least 1"
+    if kind == N.CS_LOAD_BAD_RECORD:
+        rec, a, b = int(info[4]), int(info[5]), int(info[6])
+        raw = bytes(buf[a:b].cpu().numpy() if hasattr(buf, "cpu") else buf[a:b])
+        line = raw.decode("utf-8", errors="replace")
+        kd, width = int(info[3]), int(info[1])
+        toks = line.split() if kd < 0 else [t.strip() for t in line.split(chr(kd))]
+        if len(toks) != width:
+            return f"{source}: row {rec + 1}: expected {width} values, found {len(toks)}"
+        for tok in toks:
+            try:
+                int(tok)
+            except ValueError:
+                return f"{source}: row {rec + 1}: non-integer token {tok!r}"
+        return f"{source}: row {rec + 1}: token outside the device loader's ASCII integer grammar"
+    return N.last_error()
+
+
 class GpuContext:
     """One device + one stream (cs_ctx)."""
 
@@ -61,6 +94,12 @@ class GpuContext:
         v = ctypes.c_float(0)
         check(lib.cs_ctx_last_kernel_ms(self._h, byref(v)))
         return float(v.value)
+
+    def itemset_class(self) -> str:
+        """Which class answered the last itemset_supports call: 'bitgemm', 'tensor', 'selector'."""
+        v = c_int32(0)
+        check(lib.cs_ctx_itemset_class(self._h, byref(v)))
+        return {0: "none", 1: "bitgemm", 2: "tensor", 3: "selector"}[int(v.value)]
 
     def info(self) -> dict:
         a, b, c = c_int32(), c_int32(), c_int32()
@@ -107,6 +146,46 @@ class GpuDatabase:
         h = c_void_p()
         check(lib.cs_db_create(ctx.handle, ptr(src), int(n), int(m), int(ld), ptr(ar), byref(h)))
         return cls(ctx, h, n, m, ar)
+
+    @classmethod
+    def from_text(cls, ctx: GpuContext, data, delimiter: str | None = None, arities=None,
+                  source: str = "<text>") -> "GpuDatabase":
+        """Parse delimited integer records on the device (cs_db_load_text; reference
+        ``load_csv``, database.py:160-207, same grammar, 1-based shift, errors and messages).
+
+        ``data``: bytes / uint8 numpy array (host) or a uint8 torch CUDA tensor.
+        ``delimiter``: None sniffs ',' from the first record, else one character.
+        """
+        from .database import DatabaseLoadError, UnsupportedQueryError
+
+        if isinstance(data, (bytes, bytearray, memoryview)):
+            buf = np.frombuffer(data, dtype=np.uint8)
+        else:
+            buf = data
+        nbytes = int(buf.numel() if hasattr(buf, "numel") else buf.size)
+        if delimiter is None:
+            delim = N.CS_DELIM_SNIFF
+        else:
+            raw = delimiter.encode()
+            if len(raw) != 1:
+                raise UnsupportedQueryError(
+                    f"the device loader splits on one single-byte delimiter, got {delimiter!r}")
+            delim = raw[0]
+        ar = None if arities is None else np.ascontiguousarray(list(arities), dtype=np.int32)
+        info = np.zeros(8, dtype=np.int64)
+        h = c_void_p()
+        rc = lib.cs_db_load_text(ctx.handle, ptr(buf) if nbytes else None, nbytes, int(delim),
+                                 ptr(ar) if ar is not None and len(ar) else None,
+                                 0 if ar is None else len(ar), byref(h), ptr(info))
+        if rc == N.CS_ERR_PARSE:
+            raise DatabaseLoadError(_load_message(source, buf, info, ar))
+        check(rc)
+        width = int(info[1])
+        out_ar = np.empty(width, dtype=np.int32)
+        check(lib.cs_db_arities(h, ptr(out_ar)))
+        db = cls(ctx, h, width, int(info[2]), out_ar)
+        db.load_info = {"delimiter": None if info[3] < 0 else chr(int(info[3])), "one_based": bool(info[7])}
+        return db
 
     @classmethod
     def empty(cls, ctx: GpuContext, n: int, m: int, arities) -> "GpuDatabase":

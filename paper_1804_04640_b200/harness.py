@@ -97,6 +97,40 @@ class DeviceDatabase:
         return self.gdb.download(i)
 
 
+def _read_pinned(path):
+    """File bytes in page-locked host memory when torch can provide it (the H2D copy then runs
+    as one DMA), else a plain numpy buffer (the library stages it)."""
+    import os
+
+    size = os.path.getsize(path)
+    try:
+        import torch
+
+        if size >= (8 << 20) and torch.cuda.is_available():
+            buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+            with open(path, "rb", buffering=0) as fh:
+                got = fh.readinto(memoryview(buf.numpy()))
+            if got == size:
+                return buf
+    except ImportError:
+        pass
+    return np.fromfile(str(path), dtype=np.uint8)
+
+
+def load_csv_device(path, delimiter: str | None = None, arities=None, device: int = 0) -> DeviceDatabase:
+    """``load_csv`` (reference database.py:171-207) with the parse on the device.
+
+    The file's bytes go to HBM once and are tokenised there (cs_db_load_text); the host never
+    builds the reference's int64 (m, n) matrix.  Same grammar, 1-based shift, arity inference /
+    checks and DatabaseLoadError messages as :func:`~paper_1804_04640_b200.database.load_csv`
+    for ASCII text.  The result drops into :class:`GpuStrategy` like a host ``Database``.
+    """
+    raw = _read_pinned(path)
+    gdb = GpuDatabase.from_text(shared_context(device), raw, delimiter=delimiter, arities=arities,
+                                source=str(path))
+    return DeviceDatabase(gdb)
+
+
 # fused aggregators: by exact type, ours or the reference's (duck-typed protocol)
 _FUSED_NAMES = {"LogLikelihood": "loglik", "MdlScore": "mdl", "NullSink": "nnz", "MutualInformation": "mi"}
 _FUSED_MODULES = {LogLikelihood.__module__, "countstream.aggregators"}

@@ -302,8 +302,15 @@ def test_properties_full_size(ctx):
         assert np.array_equal(t.reshape(last, -1).sum(axis=0), s)
 
 
-def test_itemset_supports_all_pairs_triples(ctx):
-    """cs_itemset_supports (Harley-Seal bit-GEMM) vs the bitmap_count restatement."""
+@pytest.fixture(params=["0", "1"], ids=["bitgemm", "selector"])
+def itemset_path(request, monkeypatch):
+    """Force the dense bit-GEMM classes (K4b/K4c) or the rarest-item selector class (K4d)."""
+    monkeypatch.setenv("CS_ITEMSETS_SEL", request.param)
+    return request.param
+
+
+def test_itemset_supports_all_pairs_triples(ctx, itemset_path):
+    """cs_itemset_supports (both classes) vs the bitmap_count restatement."""
     import itertools
 
     rng = np.random.default_rng(17)
@@ -356,7 +363,7 @@ def test_itemset_supports_wide_chunked(ctx):
             assert np.array_equal(got, t[b, b + 1:].astype(np.int64)), (a, b)
 
 
-def test_cfg4_workload_small(ctx):
+def test_cfg4_workload_small(ctx, itemset_path):
     """configs[3] generator + top-k selection + supports at reduced m."""
     w = workloads.cfg4(m=200_000, n_items=300, top=40)
     gdb = w.build_device(ctx)
@@ -528,7 +535,7 @@ def test_cfg2_full_size_sample(ctx):
     assert np.allclose(ll, oll, rtol=1e-9, atol=1e-9)
 
 
-def test_cfg4_full_m_sample(ctx):
+def test_cfg4_full_m_sample(ctx, itemset_path):
     """configs[3] at full m = 1e7: supports of all pairs/triples of 10 of the top items vs the
     bitmap_count restatement on twin-regenerated columns."""
     w = workloads.cfg4()
@@ -549,3 +556,39 @@ def test_cfg4_full_m_sample(ctx):
     pairs = list(itertools.combinations(range(len(sample)), 2))
     wantp = O.bitmap_counts(planes, [((sample[a], 1), (sample[b], 1)) for a, b in pairs], w.m)
     assert [int(pr[a, b]) for a, b in pairs] == wantp.tolist()
+
+
+def test_cfg4_full_classes_agree(ctx, monkeypatch):
+    """configs[3] in full (200 items, m = 1e7): the selector class (the bench path) and the
+    tensor-core bit-GEMM give identical pair and triple supports, and a spread of 12 items'
+    pairs/triples (indexed inside the 200-item numbering) match bitmap_count on twin columns."""
+    import itertools
+
+    w = workloads.cfg4()
+    gdb = w.build_device(ctx)
+    sup = gdb.count_points([((v,), (1,)) for v in range(w.n)])
+    top = workloads.select_top_items(sup, 200)
+    gdb.bitmap_build(top)
+    monkeypatch.setenv("CS_ITEMSETS_SEL", "1")
+    pr1, tr1 = gdb.itemset_supports(top)
+    monkeypatch.setenv("CS_ITEMSETS_SEL", "0")
+    pr0, tr0 = gdb.itemset_supports(top)
+    assert np.array_equal(np.triu(pr1, 1), np.triu(pr0, 1))
+    assert np.array_equal(tr1, tr0)
+    pick = list(range(0, 200, 17))
+    vars_ = [top[i] for i in pick]
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m), vars_)
+    planes = {(v, 1): O.bitmap_planes(cols[v], 1) for v in vars_}
+    n = 200
+
+    def tri_index(a, b, c):
+        c3 = lambda v: v * (v - 1) * (v - 2) // 6 if v >= 3 else 0  # noqa: E731
+        c2 = lambda v: v * (v - 1) // 2 if v >= 2 else 0  # noqa: E731
+        return c3(n) - c3(n - a) + c2(n - a - 1) - c2(n - b) + (c - b - 1)
+
+    tri = list(itertools.combinations(pick, 3))
+    want = O.bitmap_counts(planes, [tuple((top[x], 1) for x in t) for t in tri], w.m)
+    assert [int(tr1[tri_index(*t)]) for t in tri] == want.tolist()
+    pairs = list(itertools.combinations(pick, 2))
+    wantp = O.bitmap_counts(planes, [((top[a], 1), (top[b], 1)) for a, b in pairs], w.m)
+    assert [int(pr1[a, b]) for a, b in pairs] == wantp.tolist()
