@@ -710,6 +710,8 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
                                  200 * 1024));
     CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024));
+    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse_thr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
     attrs = true;
   }
   cudaStream_t st = ctx->stream;
@@ -808,22 +810,25 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   cudaMemsetAsync(colmax, 0x80, sizeof(int) * width, st);  // 0x80808080 < -TX_SAT
   cudaMemsetAsync(gmin, 0x7f, sizeof(int), st);            // 0x7f7f7f7f > TX_SAT
   cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st);
-  int tr = 256;
-  while (tr > 32 && 4 * width + width * (int64_t)tr > 48 * 1024) tr >>= 1;
-  const bool direct = 4 * width + width * (int64_t)tr > 200 * 1024;
-  // text staging: the tile's span (~tr records of nbytes/nrec bytes), 16-B rounded, <= 64 KB
-  const double avg = (double)nbytes / (double)nrec;
-  const int64_t tile_b = direct ? 0 : round_up(width * (int64_t)tr, 16);
-  const int32_t stage = (int32_t)std::max<int64_t>(
-      0, std::min<int64_t>(round_up((int64_t)(avg * tr * 1.25) + 64, 16), 200 * 1024 - 4 * width - tile_b));
-  const size_t smem = 4 * width + tile_b + stage;
-  const unsigned pgrid = (unsigned)((nrec + tr - 1) / tr);
-  if (direct)
-    k_txt_parse<true><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
-                                                       db->cols, db->ld, colmax, gmin, bad, stage);
-  else
-    k_txt_parse<false><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
-                                                        db->cols, db->ld, colmax, gmin, bad, stage);
+  if (width <= 256) {
+    // thread per record, SMEM tile [W][256]
+    const unsigned pgrid = (unsigned)((nrec + TX_THREADS - 1) / TX_THREADS);
+    k_txt_parse_thr<<<pgrid, TX_THREADS, width * TX_THREADS, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd,
+                                                                   db->cols, db->ld, colmax, gmin, bad);
+  } else {
+    // warp per record (long records), SMEM tile [W][tr]
+    int tr = 256;
+    while (tr > 32 && 4 * width + width * (int64_t)tr > 48 * 1024) tr >>= 1;
+    const bool direct = 4 * width + width * (int64_t)tr > 200 * 1024;
+    const size_t smem = 4 * width + (direct ? 0 : width * (int64_t)tr);
+    const unsigned pgrid = (unsigned)((nrec + tr - 1) / tr);
+    if (direct)
+      k_txt_parse<true><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
+                                                         db->cols, db->ld, colmax, gmin, bad);
+    else
+      k_txt_parse<false><<<pgrid, TX_THREADS, smem, st>>>(dt, la, lb, rec_line, nrec, (int32_t)width, kd, tr,
+                                                          db->cols, db->ld, colmax, gmin, bad);
+  }
   ctx->launches++;
   if (cudaGetLastError() != cudaSuccess) return drop(fail(CS_ERR_CUDA, "k_txt_parse launch failed"));
   unsigned long long hbad = 0;

@@ -137,9 +137,18 @@ __global__ void __launch_bounds__(TX_THREADS) k_txt_breaks(const uint8_t* __rest
   }
 }
 
+// 4 bytes -> 4-bit mask of the bytes that are not str.isspace (\t..\r, \x1c..\x20)
+__device__ __forceinline__ uint32_t tx_nonws4(uint32_t w) {
+  const uint32_t a = __vcmpleu4(__vsub4(w, 0x09090909u), 0x04040404u);
+  const uint32_t b = __vcmpleu4(__vsub4(w, 0x1c1c1c1cu), 0x04040404u);
+  const uint32_t k = ~(a | b) & 0x01010101u;  // 1 per non-whitespace byte
+  return (k * 0x00204081u) >> 21 & 0xfu;       // byte i -> bit i
+}
+
 // Warp per line: stripped bounds and the non-empty flag (str.strip, then `if ln`).  Each lane
-// takes 16 aligned bytes per step (a 512-B window per warp: one step for typical records); the
-// first / last non-whitespace byte come from per-lane 16-bit masks and a warp min / max.
+// takes 16 aligned bytes per step (a 512-B window per warp: one step for typical records);
+// SIMD byte compares give a 16-bit non-whitespace mask, clipped to the line, and the first /
+// last set byte over the warp are a min / max reduction.
 __global__ void k_txt_lines(const uint8_t* __restrict__ text, int64_t nbytes, const int64_t* __restrict__ brk,
                             int64_t nlines, int64_t* __restrict__ la, int64_t* __restrict__ lb,
                             int64_t* __restrict__ nonempty) {
@@ -154,23 +163,22 @@ __global__ void k_txt_lines(const uint8_t* __restrict__ text, int64_t nbytes, co
       uint32_t mask = 0;  // bit i: byte q + i is in [s, e) and not whitespace
       if (q < e && q + 16 > s) {
         const uint4 v = *reinterpret_cast<const uint4*>(text + q);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t c = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
-          const int64_t p = q + i;
-          if (p >= s && p < e && !tx_ws(c)) mask |= 1u << i;
-        }
+        mask = tx_nonws4(v.x) | tx_nonws4(v.y) << 4 | tx_nonws4(v.z) << 8 | tx_nonws4(v.w) << 12;
+        const int64_t lo = s - q, hi = e - q;  // keep bits [lo, hi)
+        if (lo > 0) mask &= 0xffffu << lo;
+        if (hi < 16) mask &= (1u << hi) - 1u;
       }
-      int64_t fa = mask ? q + __ffs(mask) - 1 : INT64_MAX;
-      int64_t fb = mask ? q + 32 - __clz(mask) : -1;
+      int fa = mask ? __ffs(mask) - 1 + 16 * lane : 1 << 30;
+      int fb = mask ? 16 * lane + 32 - __clz(mask) : -1;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
         fb = max(fb, __shfl_xor_sync(0xffffffffu, fb, o));
       }
-      a = min(a, fa);
-      b = max(b, fb);
+      if (fb >= 0) {
+        a = min(a, q0 + fa);
+        b = q0 + fb;
+      }
     }
     if (lane == 0) {
       const bool ne = b >= 0;
@@ -245,27 +253,15 @@ __global__ void __launch_bounds__(TX_THREADS) k_txt_parse(
     const uint8_t* __restrict__ text, const int64_t* __restrict__ la, const int64_t* __restrict__ lb,
     const int64_t* __restrict__ rec_line, int64_t nrec, int32_t width, int32_t delim, int32_t tr,
     uint8_t* __restrict__ cols, int64_t ld, int* __restrict__ colmax, int* __restrict__ gmin,
-    unsigned long long* __restrict__ bad, int32_t stage_bytes) {
+    unsigned long long* __restrict__ bad) {
   extern __shared__ __align__(16) uint8_t tx_smem[];
   int* s_max = reinterpret_cast<int*>(tx_smem);
   uint8_t* tile = tx_smem + 4 * width;
-  uint8_t* stage = tile + (DIRECT ? 0 : ((int64_t)width * tr + 15) / 16 * 16);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int c = threadIdx.x; c < width; c += blockDim.x) s_max[c] = INT_MIN;
   const int64_t r0 = (int64_t)blockIdx.x * tr;
   const int nr = (int)(nrec - r0 < tr ? nrec - r0 : tr);
-  // the tile's records are consecutive lines: stage their text span in SMEM when it fits
-  // (16-B loads), so the tokenisers below read shared memory instead of chasing global bytes
   const uint8_t* src = text;
-  {
-    const int64_t t0 = la[rec_line[r0]] & ~(int64_t)15, t1 = lb[rec_line[r0 + nr - 1]] + 1;
-    if (t1 - t0 <= stage_bytes) {
-      const int nv = (int)((t1 - t0 + 15) >> 4);
-      for (int i = threadIdx.x; i < nv; i += blockDim.x)
-        reinterpret_cast<uint4*>(stage)[i] = reinterpret_cast<const uint4*>(text + t0)[i];
-      src = stage - t0;  // src[p] = text[p] for p in [t0, t1)
-    }
-  }
   __syncthreads();
   int lmin = INT_MAX;
   for (int rr = warp; rr < nr; rr += TX_THREADS / 32) {
@@ -327,6 +323,106 @@ __global__ void __launch_bounds__(TX_THREADS) k_txt_parse(
   }
   for (int c = threadIdx.x; c < width; c += blockDim.x)
     if (s_max[c] != INT_MIN) atomicMax(colmax + c, s_max[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+  if (lane == 0 && lmin != INT_MAX) atomicMin(gmin, lmin);
+}
+
+// Thread per record (records of <= ~384 values): one pass over the record's bytes with 16-B
+// loads and a branch-free int() state machine per byte, so the 32 lanes of a warp stay
+// converged; values go to the SMEM tile [W][tr] (tr = blockDim = 256).  Column maxima are taken
+// from the tile bytes at write-out (values > 255 or < 0 also go straight to the global max /
+// min, they always end in an error).  Token grammar as tx_int; delim < 0: whitespace runs.
+enum : uint32_t { TS_START = 0, TS_SIGN = 1, TS_DIG = 2, TS_UND = 3, TS_TRAIL = 4, TS_BAD = 5 };
+
+__global__ void __launch_bounds__(TX_THREADS) k_txt_parse_thr(
+    const uint8_t* __restrict__ text, const int64_t* __restrict__ la, const int64_t* __restrict__ lb,
+    const int64_t* __restrict__ rec_line, int64_t nrec, int32_t width, int32_t delim,
+    uint8_t* __restrict__ cols, int64_t ld, int* __restrict__ colmax, int* __restrict__ gmin,
+    unsigned long long* __restrict__ bad) {
+  extern __shared__ __align__(16) uint8_t tx_smem[];
+  uint8_t* tile = tx_smem;  // [width][TX_THREADS]
+  const int tr = TX_THREADS;
+  const int64_t r0 = (int64_t)blockIdx.x * tr;
+  const int nr = (int)(nrec - r0 < tr ? nrec - r0 : tr);
+  const int rr = threadIdx.x;
+  int lmin = INT_MAX;
+  if (rr < nr) {
+    const int64_t rec = r0 + rr, ln = rec_line[rec], a = la[ln], b = lb[ln];
+    const bool wsmode = delim < 0;
+    const uint32_t dl = (uint32_t)(wsmode ? 256 : delim);
+    uint32_t st = TS_START;
+    bool in_tok = false, ok = true;
+    int v = 0, neg = 0, t = 0;
+    for (int64_t q = a & ~(int64_t)15; q <= b; q += 16) {
+      const uint4 x = *reinterpret_cast<const uint4*>(text + q);
+      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t p = q + i;
+        if (p < a || p > b) continue;
+        const uint32_t c = p == b ? 32u : (w4[i >> 2] >> (8 * (i & 3))) & 0xffu;  // b: virtual end
+        const bool end = p == b;
+        const bool ws = tx_ws(c);
+        const bool sep = end || (wsmode ? ws : c == dl);
+        const uint32_t d = c - '0';
+        const bool dig = d <= 9u;
+        if (!sep) {
+          if (wsmode) in_tok = true;
+          // next state of the token grammar (delim mode: surrounding whitespace allowed)
+          uint32_t ns;
+          if (dig) ns = (st == TS_TRAIL || st == TS_BAD) ? TS_BAD : TS_DIG;
+          else if (c == '_') ns = st == TS_DIG ? TS_UND : TS_BAD;
+          else if (c == '+' || c == '-') ns = st == TS_START ? TS_SIGN : TS_BAD;
+          else if (ws) ns = st == TS_START ? TS_START : (st == TS_DIG || st == TS_TRAIL) ? TS_TRAIL : TS_BAD;
+          else ns = TS_BAD;
+          if (c == '-' && st == TS_START) neg = 1;
+          if (dig && ns == TS_DIG) v = min(v * 10 + (int)d, TX_SAT);
+          st = ns;
+        }
+        // a field / token ends here
+        if (sep && (!wsmode || in_tok)) {
+          const bool good = st == TS_DIG || st == TS_TRAIL;
+          ok = ok && good;
+          const int val = neg ? -v : v;
+          if (good && t < width) {
+            tile[t * tr + rr] = (uint8_t)val;
+            if (val > 255) atomicMax(colmax + t, val);
+            lmin = min(lmin, val);
+          }
+          ++t;
+          st = TS_START;
+          v = 0;
+          neg = 0;
+          in_tok = false;
+        }
+      }
+    }
+    if (!ok || t != width) atomicMin(bad, (unsigned long long)rec);
+  }
+  __syncthreads();
+  // write-out: warp per tile row (column), lanes over the row's 64 words; per-column max of the
+  // bytes of real records
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = warp; t < width; t += TX_THREADS / 32) {
+    uint32_t mx = 0;
+    for (int j = lane; j < tr / 4; j += 32) {
+      uint32_t wv = *reinterpret_cast<const uint32_t*>(tile + t * tr + 4 * j);
+      const int left = nr - 4 * j;
+      if (left < 4) wv &= left <= 0 ? 0u : (1u << (8 * left)) - 1u;
+      if (left > 0) {
+        uint8_t* dst = cols + (int64_t)t * ld + r0 + 4 * j;
+        if (left >= 4) *reinterpret_cast<uint32_t*>(dst) = wv;
+        else
+          for (int q2 = 0; q2 < left; ++q2) dst[q2] = (uint8_t)(wv >> (8 * q2));
+      }
+      mx = __vmaxu4(mx, wv);
+    }
+    mx = max(max(mx & 0xffu, (mx >> 8) & 0xffu), max((mx >> 16) & 0xffu, mx >> 24));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(colmax + t, (int)mx);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
   if (lane == 0 && lmin != INT_MAX) atomicMin(gmin, lmin);

@@ -99,8 +99,9 @@ constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 //   A2  per 32-record batch: each lane gathers its record's mask words below rank r, 32
 //       ballots per mask word transpose the batch into bit words Y[b][y] (bit l = record l of
 //       the batch holds rank y)
-//   B   Gram of the batches: thread (by, bz), by <= bz, owns an 8 x 8 block of (y, z)
-//       counters in registers: acc += popc(Y[b][y] & Y[b][z])
+//   B   Gram of the batches: thread (by, bz, g), by <= bz, owns an 8 x 8 block of (y, z)
+//       counters in registers, acc += popc(Y[b][y] & Y[b][z]) over the batches b = g mod G
+//       (G = 512 / #blocks thread groups, so small-r units keep every thread busy)
 // and at the unit's end the non-zero counters with y <= z < r go to the global arrays:
 // y == z -> pair (s, y), y < z -> triple (s, y, z).  A record holding k more frequent items
 // costs ~(r/8)^2 x 64 / 32 popcounts regardless of k, so this is the dense Gram of the
@@ -126,9 +127,14 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
     const SelUnit u = units[ui];
     const int r = u.r;
     const int nb = (r + 7) >> 3;
+    // thread -> (Gram block, batch group): with few blocks (frequent selectors, small r) several
+    // threads share a block and split the batches, each keeping its own partial counters
+    const int nblk = nb * (nb + 1) / 2;
+    const int ngrp = SEL_THREADS / nblk;
+    const int grp = threadIdx.x / nblk;
     int by = -1, bz = -1;
-    {
-      int t = threadIdx.x;
+    if (grp < ngrp) {
+      int t = threadIdx.x - grp * nblk;
       for (int y = 0; y < nb; ++y) {
         if (t < nb - y) {
           by = y;
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
       __syncthreads();
       // B: Gram of the batches
       if (by >= 0) {
-        for (int b = 0; b < nbatch; ++b) {
+        for (int b = grp; b < nbatch; b += ngrp) {
           const uint4* yp = reinterpret_cast<const uint4*>(Y + b * R + 8 * by);
           const uint4* zp = reinterpret_cast<const uint4*>(Y + b * R + 8 * bz);
           const uint4 y0 = yp[0], y1 = yp[1], z0 = zp[0], z1 = zp[1];
