@@ -429,8 +429,8 @@ class ItemsetRunner:
         """K4d (rarest-item selection).  HBM roofline over its algorithmic bytes: k_sel_rowmask
         reads the k state-1 planes and writes the record-major rank masks (wr words per record);
         k_sel_gram reads each selector's plane and, per record holding the selector of rank r,
-        the ceil(r/32) mask words below r.  Its issue bound is POPC: 2 (r/8)(r/8+1)/2 x 64 / 64
-        popcounts per selected record, reported against 16 POPC/clk/SM (tools/microbench.cu)."""
+        the ceil(r/32) mask words below r.  Its issue bound is POPC: one per (8 x 4 Gram block, 32-record
+        batch) counter, reported against 16 POPC/clk/SM (tools/microbench.cu)."""
         k, m = len(self.items), self.w.m
         words = -(-(-(-m // 32)) // 32) * 32  # plane words, padded to 32
         wr = 1 if k <= 32 else 2 if k <= 64 else 4 if k <= 128 else 8
@@ -440,8 +440,9 @@ class ItemsetRunner:
         popc = 0.0
         for r, s in enumerate(supp):
             if r:
-                nb = (r + 7) // 8
-                popc += -(-s // 32) * nb * (nb + 1) / 2 * 64
+                nby, nbz = (r + 7) // 8, (r + 3) // 4
+                nblk = sum(nbz - 2 * y for y in range(nby) if 2 * y < nbz)
+                popc += -(-s // 32) * nblk * 32
         peak, src = load_peaks()
         achieved = algo / (k_ms / 1e3) / 1e9
         mhz = (clocks or {}).get("sm_mhz") or 1965.0

@@ -2040,14 +2040,16 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   std::iota(rank_item.begin(), rank_item.end(), 0);
   std::stable_sort(rank_item.begin(), rank_item.end(), [&](int a, int b) { return supp[a] > supp[b]; });
   const double m = (double)db->m;
-  // cost model: k_sel_gram issues (r/8)^2 x 2 popcounts per selected record of rank r (8 x 8
+  // cost model: k_sel_gram issues ~r^2/64 popcounts per selected record of rank r (8 x 4
   // register blocks over 32-record batches), plus the record gathers
   std::vector<double> cost(n, 0.0);
   double total = 0.0, gathered = 0.0;
   for (int r = 1; r < n; ++r) {
     const double sr = (double)supp[rank_item[r]];
-    const double nb = (r + 7) / 8;
-    cost[r] = sr * (nb * (nb + 1) + 4.0) + (double)W / 16.0;
+    const int nby = (r + 7) / 8, nbz = (r + 3) / 4;
+    double nblk = 0;
+    for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
+    cost[r] = sr * (nblk + 4.0) + (double)W / 16.0;  // nblk x 32 popc per 32-record batch
     total += cost[r];
     gathered += sr;
   }
@@ -2059,13 +2061,13 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   // 3. record-major rank masks
   const int wr = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
   // units: (rank, word range) with ~equal cost, ranges in multiples of 512 words (16 warps x 32)
-  const double target = std::max(1.0, total / (ctx->num_sms * 8.0));
+  const double target = std::max(1.0, total / (ctx->num_sms * 16.0));
   std::vector<SelUnit> units;
   std::vector<double> ucost;
   for (int r = 1; r < n; ++r) {
     if (!cost[r]) continue;
     int64_t chunks = std::max<int64_t>(1, (int64_t)std::ceil(cost[r] / target));
-    const int64_t per = round_up((W + chunks - 1) / chunks, 512);
+    const int64_t per = round_up((W + chunks - 1) / chunks, 32 * SEL_WARPS);
     for (int64_t w0 = 0; w0 < W; w0 += per) {
       units.push_back(SelUnit{r, 0, w0, std::min(W, w0 + per)});
       ucost.push_back(cost[r] * (double)(std::min(W, w0 + per) - w0) / (double)W + 64.0 * r);

@@ -25,9 +25,9 @@
 
 namespace cs {
 
-constexpr int SEL_THREADS = 512;
+constexpr int SEL_THREADS = 1024;
 constexpr int SEL_WARPS = SEL_THREADS / 32;
-constexpr int SEL_MAXN = 248;  // items (ranks) on this path: (248/8)(248/8+1)/2 = 496 Gram blocks <= 512 threads
+constexpr int SEL_MAXN = 248;  // items (ranks) on this path: <= 992 8 x 4 Gram blocks <= 1024 threads
 
 struct SelUnit {
   int32_t r;      // selector rank
@@ -49,36 +49,65 @@ __global__ void k_sel_support(const uint32_t* const* __restrict__ plane, int64_t
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(supp + blockIdx.y, (unsigned long long)c);
 }
 
-// rank_plane[k] = state-1 plane of the item of rank k (k < n); wr = words per record mask (1..8)
+// rank_plane[k] = state-1 plane of the item of rank k (k < n); wr = words per record mask (1..8).
+// Warp per 8 plane words (256 records): lane i loads the 32-B sector of rank 32 j + i for every
+// rank block j, one butterfly transpose per (word, block) leaves record 32 q + lane's mask word
+// j in lane `lane`, and each record's wr words go out as one vector store (1 KB per warp).
+__global__ void __launch_bounds__(256) k_sel_rowmask(const uint32_t* const* __restrict__ rank_plane, int n,
+                                                     int64_t words, int wr, uint32_t* __restrict__ rm);
+
+// 32 x 32 bit transpose across a warp: lane r holds row r (bit c = element (r, c)); afterwards
+// lane c holds column c (bit r = element (r, c)).  Five butterfly stages, each swapping the
+// off-diagonal j x j blocks with the partner lane r ^ j.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  uint32_t m = 0x0000ffffu;
+#pragma unroll
+  for (int j = 16; j; j >>= 1, m ^= m << j) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? (x & ~m) | ((y >> j) & m) : (x & m) | ((y << j) & ~m);
+  }
+  return x;
+}
+
 __global__ void __launch_bounds__(256) k_sel_rowmask(const uint32_t* const* __restrict__ rank_plane, int n,
                                                      int64_t words, int wr, uint32_t* __restrict__ rm) {
   const int lane = threadIdx.x & 31;
+  const int64_t ngroups = words >> 3;  // words is a multiple of 32
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < words; w += nwarps) {
-    uint32_t mine[8];
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups; g += nwarps) {
+    const int64_t w0 = g * 8;
+    uint32_t out[8][8];  // [word q][block j] for record 32 (w0 + q) + lane
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      mine[j] = 0;
       if (j < wr) {
         const int k = 32 * j + lane;
-        const uint32_t x = k < n ? __ldg(rank_plane[k] + w) : 0u;
-#pragma unroll 8
-        for (int t = 0; t < 32; ++t) {
-          const uint32_t b = __ballot_sync(0xffffffffu, (x >> t) & 1u);
-          if (lane == t) mine[j] = b;
+        uint4 a0 = make_uint4(0, 0, 0, 0), a1 = make_uint4(0, 0, 0, 0);
+        if (k < n) {
+          const uint4* src = reinterpret_cast<const uint4*>(rank_plane[k] + w0);
+          a0 = __ldg(src);
+          a1 = __ldg(src + 1);
         }
+        const uint32_t x[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) out[q][j] = warp_transpose32(x[q], lane);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) out[q][j] = 0u;
       }
     }
-    uint32_t* dst = rm + (w * 32 + lane) * wr;
-    if (wr == 8) {
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(mine[0], mine[1], mine[2], mine[3]);
-      reinterpret_cast<uint4*>(dst)[1] = make_uint4(mine[4], mine[5], mine[6], mine[7]);
-    } else if (wr == 4) {
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(mine[0], mine[1], mine[2], mine[3]);
-    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < wr) dst[j] = mine[j];
+    for (int q = 0; q < 8; ++q) {
+      uint32_t* dst = rm + ((w0 + q) * 32 + lane) * wr;
+      if (wr == 8) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(out[q][0], out[q][1], out[q][2], out[q][3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(out[q][4], out[q][5], out[q][6], out[q][7]);
+      } else if (wr == 4) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(out[q][0], out[q][1], out[q][2], out[q][3]);
+      } else if (wr == 2) {
+        reinterpret_cast<uint2*>(dst)[0] = make_uint2(out[q][0], out[q][1]);
+      } else {
+        dst[0] = out[q][0];
+      }
     }
   }
 }
@@ -96,11 +125,11 @@ constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 // range) units.  Per unit, rounds of
 //   A1  warps scan 32-word chunks of the selector's plane and append the records holding it
 //       to a CTA list (exact CAS reservations; a warp whose chunk does not fit ends the round)
-//   A2  per 32-record batch: each lane gathers its record's mask words below rank r, 32
-//       ballots per mask word transpose the batch into bit words Y[b][y] (bit l = record l of
-//       the batch holds rank y)
-//   B   Gram of the batches: thread (by, bz, g), by <= bz, owns an 8 x 8 block of (y, z)
-//       counters in registers, acc += popc(Y[b][y] & Y[b][z]) over the batches b = g mod G
+//   A2  per 32-record batch: each lane gathers its record's mask words below rank r; a warp
+//       butterfly transpose per mask word turns the batch into bit words Y[b][y] (bit l =
+//       record l of the batch holds rank y)
+//   B   Gram of the batches: thread (by, bz, g) owns an 8 x 4 block of (y, z) counters
+//       (ranks 8 by.., 4 bz..; only blocks with some y <= z) in registers, acc += popc(Y[b][y] & Y[b][z]) over the batches b = g mod G
 //       (G = 512 / #blocks thread groups, so small-r units keep every thread busy)
 // and at the unit's end the non-zero counters with y <= z < r go to the global arrays:
 // y == z -> pair (s, y), y < z -> triple (s, y, z).  A record holding k more frequent items
@@ -115,7 +144,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
   extern __shared__ __align__(16) uint32_t sel_smem[];
   uint32_t* list = sel_smem;
   uint32_t* Y = sel_smem + SEL_LCAP;
-  __shared__ int s_unit, s_cnt;
+  __shared__ int s_unit, s_cnt, s_end;
   __shared__ int16_t s_item[SEL_MAXN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < n; k += SEL_THREADS) s_item[k] = rank_item[k];
@@ -126,33 +155,39 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
     if (ui >= nunits) return;
     const SelUnit u = units[ui];
     const int r = u.r;
-    const int nb = (r + 7) >> 3;
+    // Gram blocks: 8 ranks (y) x 4 ranks (z), only blocks holding some y <= z (bz >= 2 by)
+    const int nby = (r + 7) >> 3, nbz = (r + 3) >> 2;
+    int nblk = 0;
+    for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
     // thread -> (Gram block, batch group): with few blocks (frequent selectors, small r) several
     // threads share a block and split the batches, each keeping its own partial counters
-    const int nblk = nb * (nb + 1) / 2;
     const int ngrp = SEL_THREADS / nblk;
     const int grp = threadIdx.x / nblk;
     int by = -1, bz = -1;
     if (grp < ngrp) {
       int t = threadIdx.x - grp * nblk;
-      for (int y = 0; y < nb; ++y) {
-        if (t < nb - y) {
+      for (int y = 0; y < nby; ++y) {
+        const int len = nbz - 2 * y;
+        if (t < len) {
           by = y;
-          bz = y + t;
+          bz = 2 * y + t;
           break;
         }
-        t -= nb - y;
+        t -= len;
       }
     }
-    uint32_t acc[64];
+    uint32_t acc[32];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) acc[i] = 0;
+    for (int i = 0; i < 32; ++i) acc[i] = 0;
     const int nwr = (r + 31) >> 5;
     const uint32_t lastmask = (r & 31) ? (1u << (r & 31)) - 1 : 0xffffffffu;
     const uint32_t* sp = rank_plane[r];
     int64_t wnext = u.w0 + 32 * warp;
     for (;;) {
-      if (threadIdx.x == 0) s_cnt = 0;
+      if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_end = SEL_LCAP;
+      }
       __syncthreads();
       // A1: append selected records until the range ends or a chunk does not fit
       while (wnext < u.w1) {
@@ -165,25 +200,15 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
           if (lane >= o) pre += y;
         }
         const int total = __shfl_sync(0xffffffffu, pre, 31);
-        int base = 0, ok = 1;
-        if (lane == 0) {
-          int old = *reinterpret_cast<volatile int*>(&s_cnt);
-          for (;;) {
-            if (old + total > SEL_LCAP) {
-              ok = 0;
-              break;
-            }
-            const int prev = atomicCAS(&s_cnt, old, old + total);
-            if (prev == old) {
-              base = old;
-              break;
-            }
-            old = prev;
-          }
-        }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) break;
+        // reserve with one atomicAdd; a reservation past SEL_LCAP fails (every later one does
+        // too), and the round's list ends at the smallest failed base (s_end)
+        int base = 0;
+        if (lane == 0 && total) base = atomicAdd(&s_cnt, total);
         base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + total > SEL_LCAP) {
+          if (lane == 0) atomicMin(&s_end, base);
+          break;
+        }
         int pos = base + pre - c;
         const uint32_t rec0 = (uint32_t)((wnext + lane) * 32);
         while (x) {
@@ -194,42 +219,56 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
         wnext += 32 * SEL_WARPS;
       }
       const bool done = __syncthreads_and(wnext >= u.w1);
-      const int cnt = s_cnt;
+      const int cnt = min(s_cnt, s_end);
       const int nbatch = (cnt + 31) >> 5;
       // A2: batch transposes (masks below rank r only; y in [r, R) comes out zero)
-      for (int b = warp; b < nbatch; b += SEL_WARPS) {
-        const int i = 32 * b + lane;
-        const uint32_t* mrow = rm + (int64_t)(i < cnt ? list[i] : 0) * wr;
-        uint32_t mw[8];
+      auto gather = [&](int i, uint32_t (&mw)[8]) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          mw[j] = (i < cnt && j < nwr) ? mrow[j] & (j == nwr - 1 ? lastmask : 0xffffffffu) : 0u;
+        for (int j = 0; j < 8; ++j) mw[j] = 0u;
+        if (i < cnt) {
+          const uint32_t* mrow = rm + (int64_t)list[i] * wr;
+          if (wr >= 4) {
+            const uint4 v0 = reinterpret_cast<const uint4*>(mrow)[0];
+            mw[0] = v0.x, mw[1] = v0.y, mw[2] = v0.z, mw[3] = v0.w;
+            if (nwr > 4) {
+              const uint4 v1 = reinterpret_cast<const uint4*>(mrow)[1];
+              mw[4] = v1.x, mw[5] = v1.y, mw[6] = v1.z, mw[7] = v1.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < nwr) mw[j] = mrow[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mw[j] = j < nwr ? mw[j] & (j == nwr - 1 ? lastmask : 0xffffffffu) : 0u;
+        }
+      };
+      auto emit = [&](int b, const uint32_t (&mw)[8]) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (j < nwr) {
-            uint32_t mine = 0;
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const uint32_t bal = __ballot_sync(0xffffffffu, (mw[j] >> t) & 1u);
-              if (lane == t) mine = bal;
-            }
-            if (32 * j + lane < R) Y[b * R + 32 * j + lane] = mine;
+            const uint32_t col = warp_transpose32(mw[j], lane);  // bit l: record l holds rank 32 j + lane
+            if (32 * j + lane < R) Y[b * R + 32 * j + lane] = col;
           }
         }
+      };
+      for (int b = warp; b < nbatch; b += SEL_WARPS) {
+        uint32_t m1[8];
+        gather(32 * b + lane, m1);
+        emit(b, m1);
       }
       __syncthreads();
       // B: Gram of the batches
       if (by >= 0) {
         for (int b = grp; b < nbatch; b += ngrp) {
           const uint4* yp = reinterpret_cast<const uint4*>(Y + b * R + 8 * by);
-          const uint4* zp = reinterpret_cast<const uint4*>(Y + b * R + 8 * bz);
-          const uint4 y0 = yp[0], y1 = yp[1], z0 = zp[0], z1 = zp[1];
+          const uint4 y0 = yp[0], y1 = yp[1], z0 = *reinterpret_cast<const uint4*>(Y + b * R + 4 * bz);
           const uint32_t ya[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-          const uint32_t za[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+          const uint32_t za[4] = {z0.x, z0.y, z0.z, z0.w};
 #pragma unroll
           for (int a = 0; a < 8; ++a)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[a * 8 + c] += __popc(ya[a] & za[c]);
+            for (int c = 0; c < 4; ++c) acc[a * 4 + c] += __popc(ya[a] & za[c]);
         }
       }
       __syncthreads();
@@ -241,9 +280,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int y = 8 * by + a, z = 8 * bz + c;
-          const uint32_t v = acc[a * 8 + c];
+        for (int c = 0; c < 4; ++c) {
+          const int y = 8 * by + a, z = 4 * bz + c;
+          const uint32_t v = acc[a * 4 + c];
           if (!v || y > z || z >= r) continue;
           const int iy = s_item[y];
           if (y == z) {
