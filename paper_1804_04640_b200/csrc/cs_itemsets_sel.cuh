@@ -190,8 +190,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
       }
       __syncthreads();
       // A1: append selected records until the range ends or a chunk does not fit
+      // the next chunk's selector word is loaded while this one is compacted
+      uint32_t xn = wnext < u.w1 ? sp[wnext + lane] : 0u;
       while (wnext < u.w1) {
-        uint32_t x = sp[wnext + lane];
+        uint32_t x = xn;
+        const int64_t wn2 = wnext + 32 * SEL_WARPS;
+        xn = wn2 < u.w1 ? sp[wn2 + lane] : 0u;
         const int c = __popc(x);
         int pre = c;
 #pragma unroll
