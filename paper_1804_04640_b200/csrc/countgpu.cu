@@ -2066,11 +2066,18 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   std::vector<double> ucost;
   for (int r = 1; r < n; ++r) {
     if (!cost[r]) continue;
-    int64_t chunks = std::max<int64_t>(1, (int64_t)std::ceil(cost[r] / target));
+    const int nby = (r + 7) / 8, nbz = (r + 3) / 4;
+    int nblk = 0;
+    for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
+    const int nsplit = (nblk + SEL_THREADS - 1) / SEL_THREADS;  // block ranges of <= SEL_THREADS
+    int64_t chunks = std::max<int64_t>(1, (int64_t)std::ceil(cost[r] / target / nsplit));
     const int64_t per = round_up((W + chunks - 1) / chunks, 32 * SEL_WARPS);
-    for (int64_t w0 = 0; w0 < W; w0 += per) {
-      units.push_back(SelUnit{r, 0, w0, std::min(W, w0 + per)});
-      ucost.push_back(cost[r] * (double)(std::min(W, w0 + per) - w0) / (double)W + 64.0 * r);
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const int b0 = (int)((int64_t)nblk * sp / nsplit), b1 = (int)((int64_t)nblk * (sp + 1) / nsplit);
+      for (int64_t w0 = 0; w0 < W; w0 += per) {
+        units.push_back(SelUnit{r, (int16_t)b0, (int16_t)b1, w0, std::min(W, w0 + per)});
+        ucost.push_back(cost[r] / nsplit * (double)(std::min(W, w0 + per) - w0) / (double)W + 64.0 * r);
+      }
     }
   }
   std::vector<int> order(units.size());
@@ -2112,7 +2119,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
                                                           (uint32_t*)(d + orm));
   ctx->launches++;
   if (!sorted.empty()) {
-    k_sel_gram<<<ctx->num_sms, SEL_THREADS, smem, ctx->stream>>>(
+    k_sel_gram<<<2 * ctx->num_sms, SEL_THREADS, smem, ctx->stream>>>(
         (const uint32_t* const*)(d + ors), (const uint32_t*)(d + orm), wr, (const int16_t*)(d + ori), n,
         (const SelUnit*)(d + ou), (int)sorted.size(), (int*)(d + ohd), Rw, (unsigned long long*)(d + opr),
         (unsigned long long*)(d + otr));

@@ -25,14 +25,15 @@
 
 namespace cs {
 
-constexpr int SEL_THREADS = 1024;
+constexpr int SEL_THREADS = 512;  // two CTAs per SM (64 registers per thread)
 constexpr int SEL_WARPS = SEL_THREADS / 32;
-constexpr int SEL_MAXN = 248;  // items (ranks) on this path: <= 992 8 x 4 Gram blocks <= 1024 threads
+constexpr int SEL_MAXN = 248;  // items (ranks) on this path (rank -> item table in static SMEM)
 
 struct SelUnit {
-  int32_t r;      // selector rank
-  int32_t pad;
-  int64_t w0, w1;  // plane words [w0, w1), multiples of 32
+  int32_t r;       // selector rank
+  int16_t blk0;    // Gram blocks [blk0, blk1) of this rank computed by the unit (<= SEL_THREADS)
+  int16_t blk1;
+  int64_t w0, w1;  // plane words [w0, w1), multiples of 32 x SEL_WARPS
 };
 
 __global__ void k_sel_support(const uint32_t* const* __restrict__ plane, int64_t words,
@@ -118,10 +119,10 @@ __device__ __forceinline__ int64_t sel_triple_index(int n, int a, int b, int c) 
   return c3(n) - c3(n - a) + c2(n - a - 1) - c2(n - b) + (c - b - 1);
 }
 
-constexpr int SEL_LCAP = 4096;           // compacted records per round
+constexpr int SEL_LCAP = 2048;           // compacted records per round
 constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 
-// K4d main kernel, one persistent 512-thread CTA per SM pulling (selector rank r, plane-word
+// K4d main kernel, two persistent 512-thread CTAs per SM (their barrier phases interleave) pulling (selector rank r, plane-word
 // range) units.  Per unit, rounds of
 //   A1  warps scan 32-word chunks of the selector's plane and append the records holding it
 //       to a CTA list (exact CAS reservations; a warp whose chunk does not fit ends the round)
@@ -136,7 +137,7 @@ constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 // costs ~(r/8)^2 x 64 / 32 popcounts regardless of k, so this is the dense Gram of the
 // selected records only: POPC-issue bound, no atomics, no per-record divergence.
 // dynamic SMEM: list (SEL_LCAP uint32) | Y (SEL_MAXB x R uint32), R = round_up(rmax, 8)
-__global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
+__global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
     const uint32_t* const* __restrict__ rank_plane, const uint32_t* __restrict__ rm, int wr,
     const int16_t* __restrict__ rank_item, int n, const SelUnit* __restrict__ units, int nunits,
     int* __restrict__ head, int R, unsigned long long* __restrict__ pairs,
@@ -157,15 +158,17 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_sel_gram(
     const int r = u.r;
     // Gram blocks: 8 ranks (y) x 4 ranks (z), only blocks holding some y <= z (bz >= 2 by)
     const int nby = (r + 7) >> 3, nbz = (r + 3) >> 2;
-    int nblk = 0;
-    for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
+    // this unit's Gram blocks: [blk0, blk1) of the rank's 8 x 4 blocks holding some y <= z
+    // (bz >= 2 by), enumerated by y block; ranks with more blocks than threads are split into
+    // several units over the same records
+    const int nblk = u.blk1 - u.blk0;
     // thread -> (Gram block, batch group): with few blocks (frequent selectors, small r) several
     // threads share a block and split the batches, each keeping its own partial counters
     const int ngrp = SEL_THREADS / nblk;
     const int grp = threadIdx.x / nblk;
     int by = -1, bz = -1;
     if (grp < ngrp) {
-      int t = threadIdx.x - grp * nblk;
+      int t = u.blk0 + threadIdx.x - grp * nblk;
       for (int y = 0; y < nby; ++y) {
         const int len = nbz - 2 * y;
         if (t < len) {
