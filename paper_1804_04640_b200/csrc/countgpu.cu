@@ -1016,11 +1016,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const bool knob_radix = env_int("CS_RADIX", 1) != 0;
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
-  for (int q = 0; q < nq; ++q) {
+  // classification of every query (independent per query; split over host threads for batches
+  // of >= 32K queries -- below that, spawning the threads costs what they save, measured)
+  auto classify = [&](int q) -> int {
     const int b = var_off[q], e = var_off[q + 1];
     const int k = e - b;
     if (k < 1) {
-      delete p;
       return fail(CS_ERR_INVALID, "query %d has no target variable", q);
     }
     QDesc d;
@@ -1030,12 +1031,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     for (int i = 0; i < k; ++i) {
       const int v = vars[b + i];
       if (v < 0 || v >= db->n) {
-        delete p;
         return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
       }
       for (int j = 0; j < i; ++j)
         if (vars[b + j] == v) {
-          delete p;
           return fail(CS_ERR_INVALID, "query %d repeats variable %d", q, v);
         }
       if (i < CS_MAXK) {
@@ -1043,7 +1042,6 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         d.stride[i] = (uint32_t)c;
       }
       if (c > (int64_t)(((uint64_t)1 << 63) - 1) / db->arity[v]) {
-        delete p;
         return fail(CS_ERR_UNSUPPORTED, "query %d: joint state space exceeds 2^63 cells", q);
       }
       c *= db->arity[v];
@@ -1052,7 +1050,6 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     d.base = db->cols;
     const bool sparse = c > ((int64_t)1 << max_dense);
     if (sparse && (flags & F_PARTIAL)) {
-      delete p;
       return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", q);
     }
     d.k = k;
@@ -1060,34 +1057,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     d.nbyte = std::max(nbyte, 1);
     d.mode = c <= 65536 ? 1 : 2;
     d.r_target = db->arity[vars[b]];
-    d.table_off = total;
     if (sparse) {
-      d.kind = 3;
-      cs_plan::SparseQ sq;
-      sq.q = q;
-      sq.k = k;
-      sq.rt = db->arity[vars[b]];
-      sq.C = (uint64_t)c;
-      uint64_t st = 1;
-      for (int i = 0; i < k; ++i) {
-        sq.vars.push_back(vars[b + i]);
-        sq.stride.push_back(st);
-        st *= (uint64_t)db->arity[vars[b + i]];
-      }
-      uint64_t H = 1024;
-      while (H < 2 * std::min<uint64_t>((uint64_t)m, sq.C)) H <<= 1;
-      sq.H = H;
-      p->sparse.push_back(sq);
-      c = 0;  // no dense table
+      d.kind = 3;  // hash class: descriptor built in the serial pass below
     } else if (k > CS_MAXK) {
-      d.kind = 2;
-      d.var_base = (int32_t)gvars.size();
-      int64_t s = 1;
-      for (int i = 0; i < k; ++i) {
-        gvars.push_back(vars[b + i]);
-        gstride.push_back((uint32_t)s);
-        s *= db->arity[vars[b + i]];
-      }
+      d.kind = 2;  // generic class: variable list appended in the serial pass below
     } else if (c <= 6 && c * c * c * c * 32 <= smem_words && knob_pack) {
       d.kind = 0;  // 4 rows per atomic (hist_smem_packed<K, 4>)
       d.pack = 4;
@@ -1173,8 +1146,71 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     }
     p->hq[q] = d;
     p->cells[q] = c;
+    return CS_OK;
+  };
+  {
+    const int want = env_int("CS_PLAN_THREADS", 0);  // 0 = automatic
+    const int nt = std::max(1, std::min(nq, want > 0 ? want
+                                              : nq >= 32768 ? (int)std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()))
+                                                           : 1));
+    std::vector<int> rc(nt, CS_OK), first_bad(nt, -1);
+    std::vector<std::string> msg(nt);
+    auto run = [&](int t) {
+      const int q0 = (int)((int64_t)nq * t / nt), q1 = (int)((int64_t)nq * (t + 1) / nt);
+      for (int q = q0; q < q1; ++q) {
+        const int r = classify(q);
+        if (r != CS_OK) {
+          rc[t] = r;
+          first_bad[t] = q;
+          msg[t] = g_err;  // thread-local message of this worker
+          return;
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(run, t);
+    run(0);
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < nt; ++t)
+      if (rc[t] != CS_OK) {  // the lowest query's error, as a serial pass would report it
+        delete p;
+        g_err = msg[t];
+        return rc[t];
+      }
+  }
+  // serial pass: table offsets, hash-class descriptors, generic-class variable lists
+  for (int q = 0; q < nq; ++q) {
+    QDesc& d = p->hq[q];
+    const int b = var_off[q], k = var_off[q + 1] - b;
+    d.table_off = total;
+    if (d.kind == 3) {
+      cs_plan::SparseQ sq;
+      sq.q = q;
+      sq.k = k;
+      sq.rt = db->arity[vars[b]];
+      sq.C = (uint64_t)p->cells[q];
+      uint64_t st = 1;
+      for (int i = 0; i < k; ++i) {
+        sq.vars.push_back(vars[b + i]);
+        sq.stride.push_back(st);
+        st *= (uint64_t)db->arity[vars[b + i]];
+      }
+      uint64_t H = 1024;
+      while (H < 2 * std::min<uint64_t>((uint64_t)m, sq.C)) H <<= 1;
+      sq.H = H;
+      p->sparse.push_back(sq);
+      p->cells[q] = 0;  // no dense table
+    } else if (d.kind == 2) {
+      d.var_base = (int32_t)gvars.size();
+      int64_t s2 = 1;
+      for (int i = 0; i < k; ++i) {
+        gvars.push_back(vars[b + i]);
+        gstride.push_back((uint32_t)s2);
+        s2 *= db->arity[vars[b + i]];
+      }
+    }
     p->table_off[q] = total;
-    total += c;
+    total += p->cells[q];
   }
   p->total_cells = total;
   const bool trace = env_int("CS_TRACE", 0) != 0;
@@ -1517,7 +1553,8 @@ struct OutBuf {
   void* user = nullptr;
   void* dev = nullptr;
   size_t bytes = 0;
-  bool host = false;
+  bool host = false;    // device scratch, copied to the user's host buffer at the end
+  bool mapped = false;  // the user's page-locked host buffer, written in place by the kernels
 };
 
 static int route(cs_ctx* ctx, int slot, void* user, size_t bytes, OutBuf& ob) {
@@ -1537,10 +1574,26 @@ static int plan_tables(cs_plan* p, uint32_t* user_tables, OutBuf& tb, uint32_t**
   *dtab = nullptr;
   tb = OutBuf();
   const bool user_dev = user_tables && is_device_ptr(user_tables);
+  // page-locked host tables that the kernels only ever store to (no zeroing, no global
+  // accumulation): the K1 epilogues write them directly over the bus, overlapped with the
+  // remaining histogram work, instead of a scratch table plus a D2H copy after the last kernel
+  void* mapped = nullptr;
+  if (user_tables && !user_dev && !p->needs_zero && !p->needs_global && env_int("CS_ZEROCOPY", 1)) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, user_tables) == cudaSuccess && a.type == cudaMemoryTypeHost)
+      mapped = a.devicePointer;
+    cudaGetLastError();
+  }
   if (user_dev) {
     tb.user = tb.dev = user_tables;
     tb.bytes = bytes;
     *dtab = user_tables;
+  } else if (mapped) {
+    tb.user = user_tables;
+    tb.dev = mapped;
+    tb.bytes = bytes;
+    tb.mapped = true;
+    *dtab = (uint32_t*)mapped;
   } else if (user_tables || (p->flags & F_TABLES) || p->needs_global) {
     if (p->transient) {
       void* b = nullptr;
@@ -1587,6 +1640,7 @@ static int input_tables(cs_plan* p, const uint32_t* tables, const uint32_t** out
 static int finish_outputs(cs_ctx* ctx, OutBuf* obs, int nob) {
   bool any_host = false;
   for (int i = 0; i < nob; ++i) {
+    any_host = any_host || obs[i].mapped;  // written in place by the kernels: wait for them
     if (obs[i].host) {
       CS_CUDA(cudaMemcpyAsync(obs[i].user, obs[i].dev, obs[i].bytes, cudaMemcpyDeviceToHost, ctx->stream));
       any_host = true;
@@ -2049,19 +2103,21 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
     const int nby = (r + 7) / 8, nbz = (r + 3) / 4;
     double nblk = 0;
     for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
-    cost[r] = sr * (nblk + 4.0) + (double)W / 16.0;  // nblk x 32 popc per 32-record batch
+    // warp instructions: Gram 3 x 32 popc-steps per block per 32-record batch, the batch
+    // transposes ~30 per mask word per batch, the selector-plane scan ~1.25 per word
+    cost[r] = sr * (0.094 * nblk + (r + 31) / 32 + 1.0) + 1.25 * (double)W;
     total += cost[r];
     gathered += sr;
   }
   // measured rates (B200): POPC ~16/clk/SM at ~60% issue; the tcgen05 bit-GEMM ~7e14 MAC/s
-  const double sparse_s = total / (ctx->num_sms * 16.0 * 1.9e9 * 0.6) + gathered * 32.0 / 3e12 +
+  const double sparse_s = total / (ctx->num_sms * 4.0 * 1.9e9 * 0.5) + gathered * 32.0 / 3e12 +
                           (double)W * 32 * 32 / 5e12;
   const double dense_s = ((double)ntri + 0.5 * n * (n - 1)) * m / 7e14;
   if (mode < 0 && sparse_s > dense_s) return 1;
   // 3. record-major rank masks
   const int wr = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
   // units: (rank, word range) with ~equal cost, ranges in multiples of 512 words (16 warps x 32)
-  const double target = std::max(1.0, total / (ctx->num_sms * 16.0));
+  const double target = std::max(1.0, total / (ctx->num_sms * 48.0));
   std::vector<SelUnit> units;
   std::vector<double> ucost;
   for (int r = 1; r < n; ++r) {
@@ -2076,7 +2132,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
       const int b0 = (int)((int64_t)nblk * sp / nsplit), b1 = (int)((int64_t)nblk * (sp + 1) / nsplit);
       for (int64_t w0 = 0; w0 < W; w0 += per) {
         units.push_back(SelUnit{r, (int16_t)b0, (int16_t)b1, w0, std::min(W, w0 + per)});
-        ucost.push_back(cost[r] / nsplit * (double)(std::min(W, w0 + per) - w0) / (double)W + 64.0 * r);
+        ucost.push_back(cost[r] / nsplit * (double)(std::min(W, w0 + per) - w0) / (double)W + 2.0 * (b1 - b0));
       }
     }
   }

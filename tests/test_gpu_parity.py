@@ -592,3 +592,93 @@ def test_cfg4_full_classes_agree(ctx, monkeypatch):
     pairs = list(itertools.combinations(pick, 2))
     wantp = O.bitmap_counts(planes, [((top[a], 1), (top[b], 1)) for a, b in pairs], w.m)
     assert [int(pr1[a, b]) for a, b in pairs] == wantp.tolist()
+
+
+@pytest.mark.parametrize("shape", ["two_items", "three_items", "zero_and_full", "duplicates"])
+def test_itemset_supports_edges(ctx, itemset_path, shape):
+    """Edge cases of cs_itemset_supports in both classes: n = 2 (no triples) and n = 3,
+    items that never / always occur (ties in the support ranking), an item listed twice, and
+    a row count that is not a multiple of 32."""
+    import itertools
+
+    rng = np.random.default_rng(5)
+    m = 70_001
+    n_items = 12
+    u8 = (rng.random((n_items, m)) < np.linspace(0.02, 0.6, n_items)[:, None]).astype(np.uint8)
+    u8[3] = 0  # never occurs
+    u8[7] = 1  # always occurs
+    u8[8] = u8[2]  # identical supports (tie)
+    gdb = GpuDatabase.from_columns(ctx, u8, [2] * n_items)
+    gdb.bitmap_build()
+    items = {"two_items": [5, 1], "three_items": [7, 3, 4],
+             "zero_and_full": list(range(n_items)), "duplicates": [2, 5, 2, 9, 7, 8]}[shape]
+    pr, tr = gdb.itemset_supports(items)
+    x = u8.astype(np.int64)
+    for a, b in itertools.combinations(range(len(items)), 2):
+        assert int(pr[a, b]) == int((x[items[a]] & x[items[b]]).sum()), (a, b)
+    tri = list(itertools.combinations(range(len(items)), 3))
+    assert len(tr) == len(tri)
+    for i, (a, b, c) in enumerate(tri):
+        assert int(tr[i]) == int((x[items[a]] & x[items[b]] & x[items[c]]).sum()), (a, b, c)
+
+
+def test_pinned_host_tables_written_in_place(ctx):
+    """Page-locked host tables are written by the K1 epilogues directly (zero-copy path) and
+    must equal the device-table result and the oracle; pageable ones go through scratch + D2H."""
+    import torch
+
+    w = workloads.cfg2(nq=400, m=50_000)
+    gdb = w.build_device(ctx)
+    plan = QueryPlan(gdb, w.queries, cs._native.CS_WANT_TABLES)
+    dev = torch.zeros(plan.total_cells, dtype=torch.int32, device="cuda")
+    plan.execute(tables=dev)
+    pinned = torch.zeros(plan.total_cells, dtype=torch.int32).pin_memory()
+    plan.execute(tables=pinned)
+    pageable = np.zeros(plan.total_cells, dtype=np.uint32)
+    plan.execute(tables=pageable)
+    d = dev.cpu().numpy().view(np.uint32)
+    assert np.array_equal(pinned.numpy().view(np.uint32), d)
+    assert np.array_equal(pageable, d)
+    cols = gen_twin.generate_workload_columns(w, np.arange(w.m))
+    otabs, _, _, _ = O.radix_tables(np.stack([cols[v] for v in range(w.n)]), w.arities, w.queries)
+    assert np.array_equal(d, otabs)
+
+
+def test_plan_threads_identical(ctx, monkeypatch):
+    """A 6,000-query mixed batch (SMEM, packed, radix, slice, generic > 8 variables and hash
+    classes) planned serially and on 8 host threads gives identical tables and scores; a bad
+    query deep in the batch is reported by its own index either way."""
+    rng = np.random.default_rng(31)
+    n, m = 40, 30_000
+    ar = np.concatenate([np.full(12, 2), rng.integers(3, 9, size=14), np.full(14, 8)])
+    u8 = np.stack([rng.integers(0, a, size=m) for a in ar]).astype(np.uint8)
+    gdb = GpuDatabase.from_columns(ctx, u8, ar)
+    qs = []
+    for i in range(6000):
+        if i % 997 == 0:  # 14 variables of arity 8: 8^14 > 2^30 cells, hash class
+            qs.append(tuple(int(v) for v in rng.permutation(np.arange(26, 40))))
+        elif i % 50 == 0:  # 9 or 10 binary variables: generic class (> 8 digits)
+            qs.append(tuple(int(v) for v in rng.choice(12, size=int(rng.integers(9, 11)), replace=False)))
+        else:
+            qs.append(tuple(int(v) for v in rng.choice(n, size=int(rng.integers(1, 7)), replace=False)))
+    flags = cs._native.CS_WANT_TABLES
+    out = []
+    for threads in ("1", "8"):
+        monkeypatch.setenv("CS_PLAN_THREADS", threads)
+        plan = QueryPlan(gdb, qs, flags)
+        tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+        ll = np.zeros(plan.nq)
+        nnz = np.zeros(plan.nq, dtype=np.int64)
+        plan.execute(tables=tabs, loglik=ll, nnz=nnz)
+        out.append((tabs, ll, nnz, np.asarray(plan.table_off).copy()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2])
+    assert np.array_equal(out[0][3], out[1][3])
+    bad = list(qs)
+    bad[4321] = (3, 3)
+    bad[5000] = (n + 5,)
+    for threads in ("1", "8"):
+        monkeypatch.setenv("CS_PLAN_THREADS", threads)
+        with pytest.raises(cs.InvalidQueryError, match="query 4321 repeats variable 3"):
+            QueryPlan(gdb, bad, flags)
