@@ -55,6 +55,10 @@ def database_from_args(a):
     if not a.input:
         raise ValueError("one of --input or --synthetic is required")
     ar = load_arities(a.arities) if a.arities else None
+    if getattr(a, "device_ingest", False):
+        from .harness import load_csv_device  # tokenise on the GPU (cs_db_load_text)
+
+        return load_csv_device(a.input, delimiter=a.delimiter, arities=ar)
     return load_csv(a.input, delimiter=a.delimiter, arities=ar)
 
 
@@ -165,6 +169,8 @@ def _db_flags(p):
     p.add_argument("--input", help="delimited text file of integer states, one record per line")
     p.add_argument("--delimiter", default=None, help="field delimiter (default: any whitespace)")
     p.add_argument("--arities", help="sidecar file declaring one arity per variable")
+    p.add_argument("--device-ingest", action="store_true",
+                   help="parse --input on the GPU (same grammar and errors; the data never exists on the host)")
     p.add_argument("--synthetic", metavar="n=..,m=..,arity=..", help="generate a uniform random database")
     p.add_argument("--seed", type=int, default=0, help="seed for synthetic data and query streams (default 0)")
     p.add_argument("--adtree-leaf", type=int, default=None, help="accepted for compatibility (unused)")

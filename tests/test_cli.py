@@ -84,3 +84,35 @@ def test_golden_cases_through_cli(tmp_path, reference_cases):
                              str(rr["minConfidence"]), "--max-size", str(rr["maxSize"]), "--out", str(out)]) == 0
             got = sorted(([r["antecedent"], r["consequent"]] for r in _lines(out) if r["type"] == "rule"))
             assert got == sorted([r["antecedent"], r["consequent"]] for r in rr["rules"]), name
+
+
+@pytest.mark.gpu
+def test_device_ingest_cli_matches_host_loader(tmp_path, reference_cases):
+    """`--device-ingest` (CSV tokenised on the GPU) gives the same JSONL as the host loader for
+    every golden case's database written out as a 1-based CSV: records, scores, learned parent
+    sets and rules."""
+    import numpy as np
+
+    from conftest import case_db
+
+    for name, case in reference_cases.items():
+        db = case_db(case)
+        f = tmp_path / f"{name}.csv"
+        f.write_text("\n".join(",".join(str(int(v) + 1) for v in row) for row in np.asarray(db.data).T) + "\n")
+        outs = []
+        for extra in ([], ["--device-ingest"]):
+            dbargs = ["--input", str(f), *extra]
+            res = []
+            for q in case["queries"]:
+                base = dbargs + ["--target", str(q["target"])]
+                if q["parents"]:
+                    base += ["--parents", ",".join(map(str, q["parents"]))]
+                for agg in ("records", "loglik", "mdl"):
+                    out = tmp_path / "q.jsonl"
+                    assert cli.main(["query", *base, "--agg", agg, "--out", str(out)]) == 0
+                    res.append([r for r in _lines(out) if r["type"] in ("record", "score")])
+            out = tmp_path / "l.jsonl"
+            assert cli.main(["learn-parents", *dbargs, "--max-parents", "2", "--out", str(out)]) == 0
+            res.append([r["parents"] for r in _lines(out) if r["type"] == "parent_set"])
+            outs.append(res)
+        assert outs[0] == outs[1], name
