@@ -122,6 +122,43 @@ __device__ __forceinline__ int64_t sel_triple_index(int n, int a, int b, int c) 
 constexpr int SEL_LCAP = 2048;           // compacted records per round
 constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 
+// A2 of k_sel_gram for units whose masks below rank r span NWR words: warp per 32-record
+// batch, lane l gathers record l's NWR mask words (vector loads when the row is 16-B aligned),
+// one butterfly transpose per word, Y[b][32 j + lane] = batch bits of rank 32 j + lane.
+template <int NWR>
+__device__ __forceinline__ void sel_batches(const uint32_t* __restrict__ rm, int wr, const uint32_t* list, int cnt,
+                                            int nbatch, uint32_t lastmask, int R, uint32_t* Y, int warp,
+                                            int lane) {
+  for (int b = warp; b < nbatch; b += SEL_WARPS) {
+    const int i = 32 * b + lane;
+    uint32_t mw[NWR];
+#pragma unroll
+    for (int j = 0; j < NWR; ++j) mw[j] = 0u;
+    if (i < cnt) {
+      const uint32_t* mrow = rm + (int64_t)list[i] * wr;
+      if (wr >= 4) {
+#pragma unroll
+        for (int v = 0; v < (NWR + 3) / 4; ++v) {
+          const uint4 x = reinterpret_cast<const uint4*>(mrow)[v];
+          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (4 * v + j < NWR) mw[4 * v + j] = xs[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NWR; ++j) mw[j] = mrow[j];
+      }
+      mw[NWR - 1] &= lastmask;
+    }
+#pragma unroll
+    for (int j = 0; j < NWR; ++j) {
+      const uint32_t col = warp_transpose32(mw[j], lane);  // bit l: record l holds rank 32 j + lane
+      if (32 * j + lane < R) Y[b * R + 32 * j + lane] = col;
+    }
+  }
+}
+
 // K4d main kernel, two persistent 512-thread CTAs per SM (their barrier phases interleave) pulling (selector rank r, plane-word
 // range) units.  Per unit, rounds of
 //   A1  warps scan 32-word chunks of the selector's plane and append the records holding it
@@ -147,8 +184,16 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
   uint32_t* Y = sel_smem + SEL_LCAP;
   __shared__ int s_unit, s_cnt, s_end;
   __shared__ int16_t s_item[SEL_MAXN];
+  // triple_index(n, a, b, c) = t3[a] - t2[b] + (c - b - 1) for a < b < c
+  __shared__ long long s_t3[SEL_MAXN], s_t2[SEL_MAXN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < n; k += SEL_THREADS) s_item[k] = rank_item[k];
+  for (int k = threadIdx.x; k < n; k += SEL_THREADS) {
+    s_item[k] = rank_item[k];
+    const auto c3 = [](long long x) { return x >= 3 ? x * (x - 1) * (x - 2) / 6 : 0ll; };
+    const auto c2 = [](long long x) { return x >= 2 ? x * (x - 1) / 2 : 0ll; };
+    s_t3[k] = c3(n) - c3(n - k) + c2(n - k - 1);
+    s_t2[k] = c2(n - k);
+  }
   for (;;) {
     if (threadIdx.x == 0) s_unit = atomicAdd(head, 1);
     __syncthreads();
@@ -228,41 +273,17 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
       const bool done = __syncthreads_and(wnext >= u.w1);
       const int cnt = min(s_cnt, s_end);
       const int nbatch = (cnt + 31) >> 5;
-      // A2: batch transposes (masks below rank r only; y in [r, R) comes out zero)
-      auto gather = [&](int i, uint32_t (&mw)[8]) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) mw[j] = 0u;
-        if (i < cnt) {
-          const uint32_t* mrow = rm + (int64_t)list[i] * wr;
-          if (wr >= 4) {
-            const uint4 v0 = reinterpret_cast<const uint4*>(mrow)[0];
-            mw[0] = v0.x, mw[1] = v0.y, mw[2] = v0.z, mw[3] = v0.w;
-            if (nwr > 4) {
-              const uint4 v1 = reinterpret_cast<const uint4*>(mrow)[1];
-              mw[4] = v1.x, mw[5] = v1.y, mw[6] = v1.z, mw[7] = v1.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (j < nwr) mw[j] = mrow[j];
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mw[j] = j < nwr ? mw[j] & (j == nwr - 1 ? lastmask : 0xffffffffu) : 0u;
-        }
-      };
-      auto emit = [&](int b, const uint32_t (&mw)[8]) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j < nwr) {
-            const uint32_t col = warp_transpose32(mw[j], lane);  // bit l: record l holds rank 32 j + lane
-            if (32 * j + lane < R) Y[b * R + 32 * j + lane] = col;
-          }
-        }
-      };
-      for (int b = warp; b < nbatch; b += SEL_WARPS) {
-        uint32_t m1[8];
-        gather(32 * b + lane, m1);
-        emit(b, m1);
+      // A2: batch transposes (masks below rank r only; y in [r, R) comes out zero), unrolled
+      // for the unit's mask-word count
+      switch (nwr) {
+        case 1: sel_batches<1>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 2: sel_batches<2>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 3: sel_batches<3>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 4: sel_batches<4>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 5: sel_batches<5>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 6: sel_batches<6>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        case 7: sel_batches<7>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
+        default: sel_batches<8>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
       }
       __syncthreads();
       // B: Gram of the batches
@@ -300,7 +321,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
             if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
             if (p1 > p2) { const int t = p1; p1 = p2; p2 = t; }
             if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
-            atomicAdd(triples + sel_triple_index(n, p0, p1, p2), (unsigned long long)v);
+            atomicAdd(triples + (s_t3[p0] - s_t2[p1] + (p2 - p1 - 1)), (unsigned long long)v);
           }
         }
     }
