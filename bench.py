@@ -254,6 +254,10 @@ class QueryRunner:
         self.flags = flags
         self.plan = QueryPlan(self.gdb, self.queries, flags)
         self.units = self.plan.nq
+        if self.sharded:
+            from paper_1804_04640_b200.parallel import PipelinedInstanceSharded
+
+            self.pipe = PipelinedInstanceSharded(self.gdb, self.queries, nbatch=4)
         dev = "cuda"
         self.tables = (torch.empty(max(self.plan.total_cells, 1), dtype=torch.int32, device=dev)
                        if (self.want_tables or self.sharded) else None)
@@ -275,11 +279,9 @@ class QueryRunner:
 
     def step(self):
         if self.sharded:
-            from paper_1804_04640_b200.parallel import merge_tables_
-
-            self.plan.execute(tables=self.tables)
-            merge_tables_(self.tables)  # NCCL all-reduce; uint32 sum == int32 sum bitwise
-            self.plan.score(self.tables, loglik=self.ll, mi=self.mi)
+            # four query slices: slice b's NCCL all-reduce (uint32 sum == int32 sum bitwise)
+            # overlaps slice b+1's scan; each slice is scored after its merge
+            self.pipe.run(loglik=self.ll, mi=self.mi)
         else:
             self.plan.execute(tables=self.tables, loglik=self.ll, mi=self.mi)
 

@@ -1018,6 +1018,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
   // classification of every query (independent per query; split over host threads for batches
   // of >= 32K queries -- below that, spawning the threads costs what they save, measured)
+  const double trs = now_ms();
   auto classify = [&](int q) -> int {
     const int b = var_off[q], e = var_off[q + 1];
     const int k = e - b;
@@ -1178,6 +1179,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         return rc[t];
       }
   }
+  const double trp = now_ms();
   // serial pass: table offsets, hash-class descriptors, generic-class variable lists
   for (int q = 0; q < nq; ++q) {
     QDesc& d = p->hq[q];
@@ -1436,7 +1438,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   }
   const double tr2 = trace ? now_ms() : 0.0;
   if (trace)
-    fprintf(stderr, "plan_build: classify %.3f ms, items %.3f ms, order %.3f ms\n", tr0 - trc, tr1 - tr0,
+    fprintf(stderr, "plan_build: setup %.3f ms, classify %.3f ms (parallel part %.3f), items %.3f ms, order %.3f ms\n",
+            trs - trc, tr0 - trs, trp - trs, tr1 - tr0,
             tr2 - tr1);
   // upload descriptors (one blob through pinned staging)
   CS_CUDA(cudaSetDevice(ctx->device));

@@ -112,3 +112,54 @@ class InstanceShardedPlan:
         merge_tables_(self.tables, self.group)
         self.plan.score(self.tables, loglik=loglik, mi=mi, nnz=nnz)
         return self.tables
+
+
+class PipelinedInstanceSharded:
+    """Instance-sharded batch in ``nbatch`` query slices whose merges overlap the next slice's
+    scan (survey 8(e)): slice b's partial tables are all-reduced asynchronously (NCCL runs on
+    its own stream after the compute stream's work so far) while slice b+1 is counted; slice
+    b is scored once its merge is waited on.  Results are identical to
+    :class:`InstanceShardedPlan` over the whole batch (counts are additive, scoring is per
+    query).  As for every torch.distributed call here, the library context's stream must be
+    torch's current stream (``ctx.set_stream(torch.cuda.current_stream().cuda_stream)`` under
+    ``torch.cuda.stream(s)``), so the collectives are ordered after the kernels that feed them.
+    """
+
+    def __init__(self, gdb, queries, nbatch: int = 4, torch_device="cuda", group=None):
+        import torch
+
+        from . import _native as N
+        from .engine import QueryPlan
+
+        qs = list(queries)
+        nbatch = max(1, min(nbatch, len(qs)))
+        cuts = [len(qs) * i // nbatch for i in range(nbatch + 1)]
+        self.slices = [(cuts[i], cuts[i + 1]) for i in range(nbatch) if cuts[i + 1] > cuts[i]]
+        self.plans = [QueryPlan(gdb, qs[a:b], N.CS_PARTIAL | N.CS_WANT_TABLES) for a, b in self.slices]
+        self.tables = [torch.empty(max(p.total_cells, 1), dtype=torch.int32, device=torch_device)
+                       for p in self.plans]
+        self.nq = len(qs)
+        self.group = group
+
+    def run(self, loglik=None, mi=None, nnz=None):
+        """loglik / mi / nnz: device tensors over the whole batch (or None)."""
+        import torch.distributed as dist
+
+        def part(x, a, b):
+            return None if x is None else x[a:b]
+
+        pending = None
+        for i, (plan, tab) in enumerate(zip(self.plans, self.tables)):
+            plan.execute(tables=tab)
+            work = dist.all_reduce(tab, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            if pending is not None:
+                j, w = pending
+                w.wait()  # the compute stream waits for slice j's merge, after slice i's scan
+                a, b = self.slices[j]
+                self.plans[j].score(self.tables[j], loglik=part(loglik, a, b), mi=part(mi, a, b),
+                                    nnz=part(nnz, a, b))
+            pending = (i, work)
+        j, w = pending
+        w.wait()
+        a, b = self.slices[j]
+        self.plans[j].score(self.tables[j], loglik=part(loglik, a, b), mi=part(mi, a, b), nnz=part(nnz, a, b))

@@ -682,3 +682,37 @@ def test_plan_threads_identical(ctx, monkeypatch):
         monkeypatch.setenv("CS_PLAN_THREADS", threads)
         with pytest.raises(cs.InvalidQueryError, match="query 4321 repeats variable 3"):
             QueryPlan(gdb, bad, flags)
+
+
+def test_pipelined_instance_sharded_single_rank(ctx):
+    """The pipelined instance-sharded runner (partial tables, async NCCL all-reduce overlapped
+    with the next slice's scan, per-slice scoring) on a one-rank NCCL group equals the plain
+    plan's fused LL / MI."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1804_04640_b200.parallel import PipelinedInstanceSharded
+
+    w = workloads.cfg2(nq=300, m=40_000)
+    gdb = w.build_device(ctx)
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
+    s = torch.cuda.Stream()
+    ctx.set_stream(s.cuda_stream)  # library kernels and NCCL ordered on one stream
+    try:
+        with torch.cuda.stream(s):
+            ll = torch.zeros(len(w.queries), dtype=torch.float64, device="cuda")
+            mi = torch.zeros_like(ll)
+            PipelinedInstanceSharded(gdb, w.queries, nbatch=4).run(loglik=ll, mi=mi)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_stream(None)  # back to a library-owned stream
+        if own:
+            dist.destroy_process_group()
+    plan = QueryPlan(gdb, w.queries, 0)
+    ll0 = np.zeros(plan.nq)
+    mi0 = np.zeros(plan.nq)
+    plan.execute(loglik=ll0, mi=mi0)
+    assert np.allclose(ll.cpu().numpy(), ll0, rtol=1e-12, atol=1e-9)
+    assert np.allclose(mi.cpu().numpy(), mi0, rtol=1e-9, atol=1e-12)
