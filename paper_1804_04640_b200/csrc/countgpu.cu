@@ -1016,8 +1016,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const bool knob_radix = env_int("CS_RADIX", 1) != 0;
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
-  // classification of every query (independent per query; split over host threads for batches
-  // of >= 32K queries -- below that, spawning the threads costs what they save, measured)
+  // classification of every query (independent per query)
   const double trs = now_ms();
   auto classify = [&](int q) -> int {
     const int b = var_off[q], e = var_off[q + 1];
@@ -1150,10 +1149,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     return CS_OK;
   };
   {
-    const int want = env_int("CS_PLAN_THREADS", 0);  // 0 = automatic
-    const int nt = std::max(1, std::min(nq, want > 0 ? want
-                                              : nq >= 32768 ? (int)std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()))
-                                                           : 1));
+    // host threads for the classification (CS_PLAN_THREADS, default 1): the parallel part
+    // scales (74.5K queries: 2.95 -> 0.75 ms on 8 threads) but the passes after it then read
+    // descriptors written on other cores and lose more than that (measured, tools/plan_probe.py)
+    const int nt = std::max(1, std::min(nq, env_int("CS_PLAN_THREADS", 1)));
     std::vector<int> rc(nt, CS_OK), first_bad(nt, -1);
     std::vector<std::string> msg(nt);
     auto run = [&](int t) {
