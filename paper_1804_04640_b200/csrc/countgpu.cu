@@ -81,20 +81,22 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-// K1 variants: kHist[k-1][path][nibble layout] (nullptr where a path needs fewer digits)
+// K1 variants: kHist[k-1][path][column layout: uint8 / 4-bit / 2-bit] (nullptr where a path needs fewer digits)
 using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32_t*, double*, double*,
                         int64_t*, uint32_t, double);
+#define CS_HK3(K, P) {k_hist<K, P, 0>, k_hist<K, P, 1>, k_hist<K, P, 2>}
 #define CS_HK(K)                                                                           \
-  {{k_hist<K, P_LANE16, false>, k_hist<K, P_LANE16, true>},                                \
-   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, false> : nullptr,                           \
-    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, true> : nullptr},                           \
-   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, false> : nullptr,                           \
-    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, true> : nullptr},                           \
-   {k_hist<K, P_ROWS, false>, k_hist<K, P_ROWS, true>},                                   \
-   {k_hist<K, P_HALF, false>, k_hist<K, P_HALF, true>},                                   \
-   {k_hist<K, P_SLICE, false>, k_hist<K, P_SLICE, true>}}
-static const HistFn kHist[CS_MAXK][6][2] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
+  {CS_HK3(K, P_LANE16),                                                                    \
+   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, 0> : nullptr,                               \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, 1> : nullptr,                               \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK2, 2> : nullptr},                              \
+   {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 0> : nullptr,                               \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 1> : nullptr,                               \
+    K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 2> : nullptr},                              \
+   CS_HK3(K, P_ROWS), CS_HK3(K, P_HALF), CS_HK3(K, P_SLICE)}
+static const HistFn kHist[CS_MAXK][6][3] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
+#undef CS_HK3
 #undef CS_HK
 
 // K1r partition kernels per digit count (k >= 2)
@@ -166,6 +168,8 @@ struct cs_db {
   uint8_t* cols = nullptr;
   uint8_t* nib = nullptr;  // 4-bit copy (all arities <= 16), ldn bytes per column
   int64_t ldn = 0;
+  uint8_t* crumb = nullptr;  // 2-bit copy (all arities <= 4), ldc bytes per column
+  int64_t ldc = 0;
   int32_t* d_arity = nullptr;
   std::vector<int32_t> arity;
   // bitmap index
@@ -420,12 +424,32 @@ static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, c
       CS_CUDA(cudaMemsetAsync(db->nib, 0, (size_t)n * db->ldn, ctx->stream));
     }
   }
+  // 2-bit copy when every arity <= 4 (the histogram kernels' smallest row footprint)
+  bool tiny = env_int("CS_CRUMB", 1) != 0;
+  for (int i = 0; i < n && tiny; ++i) tiny = arities[i] <= 4;
+  if (tiny) {
+    db->ldc = round_up((m + 3) / 4, 256);
+    if (cudaMalloc(&db->crumb, (size_t)n * db->ldc) != cudaSuccess) {
+      cudaGetLastError();
+      db->crumb = nullptr;
+      db->ldc = 0;
+    } else {
+      CS_CUDA(cudaMemsetAsync(db->crumb, 0, (size_t)n * db->ldc, ctx->stream));
+    }
+  }
   *out = db;
   return CS_OK;
 }
 
 // (re)pack columns [var0, var0 + nvars) into the 4-bit copy
 static int db_pack(cs_db* db, int32_t var0, int32_t nvars) {
+  if (db->crumb && nvars > 0) {
+    const int64_t w16 = (db->m + 15) >> 4;
+    dim3 g2((unsigned)std::min<int64_t>((w16 + 255) / 256, 2048), (unsigned)std::min(nvars, 1024));
+    k_pack2<<<g2, 256, 0, db->ctx->stream>>>(db->cols, db->ld, db->crumb, db->ldc, db->m, var0, nvars);
+    db->ctx->launches++;
+    CS_CUDA(cudaGetLastError());
+  }
   if (!db->nib || nvars <= 0) return CS_OK;
   cs_ctx* ctx = db->ctx;
   const int64_t words = (db->m + 7) >> 3;
@@ -536,6 +560,7 @@ extern "C" int cs_db_destroy(cs_db* db) {
   cudaStreamSynchronize(db->ctx->stream);
   if (db->cols) cudaFree(db->cols);
   if (db->nib) cudaFree(db->nib);
+  if (db->crumb) cudaFree(db->crumb);
   if (db->d_arity) cudaFree(db->d_arity);
   if (db->planes) cudaFree(db->planes);
   delete db;
@@ -907,6 +932,12 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   }
   db->arity = ar;
   CS_CUDA(cudaMemcpyAsync(db->d_arity, ar.data(), sizeof(int32_t) * width, cudaMemcpyHostToDevice, st));
+  if (db->crumb && *std::max_element(ar.begin(), ar.end()) > 4) {
+    CS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(db->crumb);
+    db->crumb = nullptr;
+    db->ldc = 0;
+  }
   if (db->nib && *std::max_element(ar.begin(), ar.end()) > 16) {
     CS_CUDA(cudaStreamSynchronize(st));
     cudaFree(db->nib);
@@ -1139,7 +1170,11 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         }
       }
     }
-    if (d.kind == 0 && db->nib && (d.pack > 1 || d.mode <= 1) && knob_nibble) {
+    if (d.kind == 0 && db->crumb && (d.pack > 1 || d.mode <= 1) && knob_nibble) {
+      d.nib = 2;  // 2-bit columns: 64 rows per 16 B
+      d.base = db->crumb;
+      for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldc / 256));
+    } else if (d.kind == 0 && db->nib && (d.pack > 1 || d.mode <= 1) && knob_nibble) {
       d.nib = 1;
       d.base = db->nib;
       for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
@@ -1305,18 +1340,18 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   }
   // SMEM-class items grouped by K1 variant (k, path, layout), groups by descending total cost,
   // LPT order inside a group; then the global-class items.
-  std::vector<std::vector<int>> groups(CS_MAXK * 16);  // key = (k-1)*16 + path*2 + nib
-  std::vector<double> gcost(CS_MAXK * 16, 0.0);
+  std::vector<std::vector<int>> groups(CS_MAXK * 24);  // key = (k-1)*24 + path*3 + layout
+  std::vector<double> gcost(CS_MAXK * 24, 0.0);
   {
     std::vector<int32_t> qkey(nq);
-    std::vector<int32_t> gsize(CS_MAXK * 16, 0);
+    std::vector<int32_t> gsize(CS_MAXK * 24, 0);
     for (int q = 0; q < nq; ++q) {
       const QDesc& d = p->hq[q];
-      qkey[q] = d.kind == 0 ? (d.k - 1) * 16 + hist_path(d) * 2 + d.nib : -1;
+      qkey[q] = d.kind == 0 ? (d.k - 1) * 24 + hist_path(d) * 3 + d.nib : -1;
     }
     for (const WItem& w : items)
       if (qkey[w.q] >= 0) gsize[qkey[w.q]]++;
-    for (int k = 0; k < CS_MAXK * 16; ++k) groups[k].reserve(gsize[k]);
+    for (int k = 0; k < CS_MAXK * 24; ++k) groups[k].reserve(gsize[k]);
     for (size_t i = 0; i < order.size(); ++i) {
       const int key = qkey[items[order[i]].q];
       if (key < 0) continue;
@@ -1332,7 +1367,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   sorted.reserve(items.size());
   for (int key : keys) {
     auto& g = groups[key];
-    if ((key % 16) / 2 == P_SLICE) {
+    if ((key % 24) / 3 == P_SLICE) {
       // slices of one segment back to back (they share its columns through L2), queries LPT
       std::map<int, double> qc;
       for (int i : g) qc[items[i].q] += cost[i];
@@ -1812,7 +1847,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   if (p->nitems > 0) {
     for (size_t g = 0; g < p->groups.size(); ++g) {
       const auto& G = p->groups[g];
-      const int k = G.key / 16 + 1, path = (G.key % 16) / 2, nib = G.key % 2;
+      const int k = G.key / 24 + 1, path = (G.key % 24) / 3, nib = G.key % 3;
       HistFn f = kHist[k - 1][path][nib];
       if (!f) return fail(CS_ERR_INVALID, "internal: no K1 variant for k=%d path=%d", k, path);
       const int grid = std::min(ctx->hist_ctas, G.count);

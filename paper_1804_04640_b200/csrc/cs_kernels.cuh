@@ -280,15 +280,28 @@ __device__ __forceinline__ void load_vec16(uint32_t (&x)[K][4], const uint8_t* p
   }
 }
 
+// Column layouts: NIB = 0 uint8 (16 rows per 16-B vector), 1 4-bit (32 rows), 2 2-bit (64 rows;
+// every arity <= 4: byte j of the copy holds rows 4j..4j+3, row 4j+i in bits 2i..2i+1).
+__host__ __device__ constexpr int rows_per_vec(int layout) { return layout == 2 ? 64 : layout == 1 ? 32 : 16; }
+__host__ __device__ constexpr int row_shift(int layout) { return layout == 2 ? 2 : layout == 1 ? 1 : 0; }
+
 // Word views of one loaded 16-byte vector per column: 4 words of 4 byte-lane rows (uint8
-// layout), or 8 words (nibble layout: low nibbles = even rows, high nibbles = odd rows, each
-// widened to byte lanes with one LOP3 / SHF+LOP3).  Row order inside a vector is irrelevant
-// to counting.
-template <int K, bool NIB, class WordFn>
+// layout), 8 words (nibble layout: low nibbles = even rows, high nibbles = odd rows, each
+// widened to byte lanes with one LOP3 / SHF+LOP3), or 16 words (2-bit layout: one SHF+LOP3
+// per view).  Row order inside a vector is irrelevant to counting.
+template <int K, int NIB, class WordFn>
 __device__ __forceinline__ void for_words(const uint32_t (&x)[K][4], WordFn f) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    if (!NIB) {
+    if (NIB == 2) {
+#pragma unroll
+      for (int sh = 0; sh < 8; sh += 2) {
+        uint32_t w[K];
+#pragma unroll
+        for (int v = 0; v < K; ++v) w[v] = (x[v][j] >> sh) & 0x03030303u;
+        f(w);
+      }
+    } else if (!NIB) {
       uint32_t w[K];
 #pragma unroll
       for (int v = 0; v < K; ++v) w[v] = x[v][j];
@@ -306,11 +319,11 @@ __device__ __forceinline__ void for_words(const uint32_t (&x)[K][4], WordFn f) {
   }
 }
 
-template <int K, bool NIB>
+template <int K, int NIB>
 __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int64_t r1,
                                                  uint32_t* sh) {
-  constexpr int RPV = NIB ? 32 : 16;  // rows per 16-byte vector
-  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  constexpr int RPV = rows_per_vec(NIB);  // rows per 16-byte vector
+  const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -369,11 +382,11 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
 // scheduled back to back so the segment's columns come from L2 after the first read.  Index =
 // digits 0..K-2 in 16-bit lanes; the last digit is compared in byte lanes (vcmpeq4) and gates
 // the atomic.  Zero padding rows fall in slice 0, cell 0 and are subtracted there.
-template <int K, bool NIB>
+template <int K, int NIB>
 __device__ __forceinline__ void hist_smem_slice(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
                                                 uint32_t slice, uint32_t nsl) {
-  constexpr int RPV = NIB ? 32 : 16;
-  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  constexpr int RPV = rows_per_vec(NIB);
+  const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -430,11 +443,11 @@ __device__ __forceinline__ void hist_smem_slice(const QDesc& q, int64_t r0, int6
 // c & 1, of its replica), which doubles the replica count R that fits -- R = 32 (lane-private,
 // bank-conflict-free) up to 3520 cells instead of 1760.  The host enables it only when a
 // counter cannot overflow: rows per item <= 65535 * R (each replica serves rows / R rows).
-template <int K, bool NIB>
+template <int K, int NIB>
 __device__ __forceinline__ void hist_smem_half(const QDesc& q, int64_t r0, int64_t r1,
                                                uint32_t* sh) {
-  constexpr int RPV = NIB ? 32 : 16;
-  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  constexpr int RPV = rows_per_vec(NIB);
+  const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -490,11 +503,11 @@ __device__ __forceinline__ void hist_smem_half(const QDesc& q, int64_t r0, int64
 // SMEM class, tables too large for 16-bit byte offsets (C*R*4 > 64 KB, C <= 65536): the
 // joint index is built in 16-bit lanes, and each row's counter address is one IMAD
 // (idx * 4R + 4 rep + base).
-template <int K, bool NIB>
+template <int K, int NIB>
 __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int64_t r1,
                                                  uint32_t* sh) {
-  constexpr int RPV = NIB ? 32 : 16;
-  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  constexpr int RPV = rows_per_vec(NIB);
+  const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -549,11 +562,11 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
 // tuple index  b0 + C b1 (+ C^2 b2 + C^3 b3)  of a C^PACK-cell table (32 replicas), so the
 // SMEM atomic traffic drops PACK-fold; the epilogue marginalises the tuple table back to the
 // C cells.  Padding rows (zeros) are subtracted from cell 0 in the epilogue.
-template <int K, int PACK, bool NIB>
+template <int K, int PACK, int NIB>
 __device__ __forceinline__ void hist_smem_packed(const QDesc& q, int64_t r0, int64_t r1,
                                                  uint32_t* sh) {
-  constexpr int RPV = NIB ? 32 : 16;
-  const uint8_t* rowp = q.base + (NIB ? (r0 >> 1) : r0);
+  constexpr int RPV = rows_per_vec(NIB);
+  const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
   uint32_t co[K], st[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
@@ -699,7 +712,7 @@ __device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0,
 enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4, P_SLICE = 5 };
 constexpr int CS_HIST_THREADS = 1024;
 
-template <int K, int PATH, bool NIB>
+template <int K, int PATH, int NIB>
 __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     k_hist(const QDesc* __restrict__ qd, const WItem* __restrict__ items, int nitems,
            int* __restrict__ head, uint32_t* tables, uint32_t* __restrict__ done, double* ll_out,
@@ -764,7 +777,7 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        const int64_t nrows = wi.r1 - wi.r0, rpv = NIB ? 32 : 16;
+        const int64_t nrows = wi.r1 - wi.r0, rpv = rows_per_vec(NIB);
         s_marg[0] -= (uint32_t)((nrows + rpv - 1) / rpv * rpv - nrows);  // zero padding rows
       }
       __syncthreads();
@@ -1182,6 +1195,32 @@ __global__ void k_pack4(const uint8_t* __restrict__ cols, int64_t ld, uint8_t* _
       lo = (lo | (lo >> 8)) & 0x0000ffffu;
       hi = (hi | (hi >> 8)) & 0x0000ffffu;
       o[w] = lo | (hi << 16);
+    }
+  }
+}
+
+// 2-bit copy of columns (every arity <= 4): output word w (rows 16w..16w+15) holds row
+// 16w + 4b + i in bits 8b + 2i .. +1 (byte b = rows 16w+4b..+3) -- the view order for_words<.., 2>
+// extracts
+__global__ void k_pack2(const uint8_t* __restrict__ cols, int64_t ld, uint8_t* __restrict__ crumb,
+                        int64_t ldc, int64_t m, int32_t var0, int32_t nvars) {
+  const int64_t words = (m + 15) >> 4;
+  for (int vv = blockIdx.y; vv < nvars; vv += gridDim.y) {
+    const uint8_t* c = cols + (int64_t)(var0 + vv) * ld;
+    uint32_t* o = reinterpret_cast<uint32_t*>(crumb + (int64_t)(var0 + vv) * ldc);
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (int64_t)gridDim.x * blockDim.x) {
+      const uint4 b = *reinterpret_cast<const uint4*>(c + 16 * w);  // 16 states, each < 4
+      const uint32_t in[4] = {b.x, b.y, b.z, b.w};  // in[b] byte i = row 16w + 4b + i
+      uint32_t out = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t x = in[q] & 0x03030303u;
+        x = (x | (x >> 6)) & 0x000f000fu;  // [r0 | r1<<2, r2 | r3<<2] in 16-bit lanes
+        x = (x | (x >> 12)) & 0xffu;       // r0 | r1<<2 | r2<<4 | r3<<6
+        out |= x << (8 * q);
+      }
+      o[w] = out;
     }
   }
 }
