@@ -128,6 +128,7 @@ struct cs_ctx {
   bool ev_valid = false;
   int64_t launches = 0;
   int32_t itemset_class = 0;  // class of the last cs_itemset_supports call (CS_ITEMSETS_*)
+  int smem_optin = 0;         // max dynamic SMEM per block (opt-in)
   // grow-only device scratch for host-bound outputs
   std::map<int, std::pair<void*, size_t>> scratch;
   // grow-only pinned staging
@@ -176,6 +177,7 @@ struct cs_db {
   uint32_t* planes = nullptr;
   int64_t words = 0;
   std::vector<int64_t> plane_off;  // per var, first plane (state 0) offset in words, -1 = none
+  std::vector<int64_t> plane_count;  // popcount of every plane (BitmapIndex.state_counts, bitmap.py:62)
 };
 
 struct cs_plan {
@@ -301,6 +303,25 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   for (RadixPartFn f : kRadixPart)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
+  {  // keep freed ingest scratch in the device's stream-ordered pool between loads
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
+  // the other large-SMEM kernels (function attributes are per device: set them per context)
+  c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_itemsets_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               c->smem_optin - 2048));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_sel_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse_thr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024));
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
   c->hist_ctas = per_sm * c->num_sms;
@@ -729,27 +750,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
     return fail(CS_ERR_PARSE, "no records found");
   }
   CS_CUDA(cudaSetDevice(ctx->device));
-  static bool attrs = false;
-  if (!attrs) {
-    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    CS_CUDA(cudaFuncSetAttribute((const void*)k_txt_parse_thr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    attrs = true;
-  }
   cudaStream_t st = ctx->stream;
-  static bool pool_kept = false;
-  if (!pool_kept) {  // keep freed scratch in the stream-ordered pool between loads
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-    pool_kept = true;
-  }
   TmpBag bag(st);
   // 1. text on the device, zero padded (vector loads and the look-ahead byte stay in bounds)
   const int64_t tbytes = round_up(nbytes, 64) + TX_PAD;
@@ -1000,7 +1001,19 @@ extern "C" int cs_bitmap_build(cs_db* db, int32_t nvars, const int32_t* vars) {
                                                  db->planes, words);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
+  // per-plane record counts (the index's state counts): the itemset planner ranks items by them
+  const int64_t nplanes = total / words;
+  unsigned long long* d_cnt = nullptr;
+  CS_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long) * nplanes));
+  CS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * nplanes, ctx->stream));
+  k_plane_popc<<<dim3(8, (unsigned)nplanes), 256, 0, ctx->stream>>>(db->planes, words, d_cnt);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  db->plane_count.assign(nplanes, 0);
+  CS_CUDA(cudaMemcpyAsync(db->plane_count.data(), d_cnt, sizeof(int64_t) * nplanes, cudaMemcpyDeviceToHost,
+                          ctx->stream));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_cnt);
   cudaFree(d_vars);
   cudaFree(d_off);
   return CS_OK;
@@ -2103,29 +2116,18 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   cs_ctx* ctx = db->ctx;
   const int64_t W = db->words;  // multiple of 32 words
   const int64_t ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
-  // 1. item supports
-  const size_t bp = sizeof(void*) * n;
+  // 1. item supports: the state-1 plane counts recorded when the bitmap index was built
   size_t off = 0;
   auto place = [&](size_t b) {
     size_t o = off;
     off = round_up(off + b, 256);
     return o;
   };
-  const size_t op = place(bp), ors = place(bp), osu = place(sizeof(unsigned long long) * n),
-               ori = place(sizeof(int16_t) * SEL_MAXN), ohd = place(sizeof(int));
+  const size_t bp = sizeof(void*) * n;
+  const size_t ors = place(bp), ori = place(sizeof(int16_t) * SEL_MAXN), ohd = place(sizeof(int));
   const size_t meta_end = off;
-  void* blob = nullptr;
-  CS_TRY(ctx->scratch_get(11, off, &blob));
-  char* d = (char*)blob;
-  CS_CUDA(cudaMemcpyAsync(d + op, hp.data(), bp, cudaMemcpyHostToDevice, ctx->stream));
-  CS_CUDA(cudaMemsetAsync(d + osu, 0, sizeof(unsigned long long) * n, ctx->stream));
-  k_sel_support<<<dim3(8, n), 256, 0, ctx->stream>>>((const uint32_t* const*)(d + op), W,
-                                                     (unsigned long long*)(d + osu));
-  ctx->launches++;
-  CS_CUDA(cudaGetLastError());
   std::vector<unsigned long long> supp(n);
-  CS_CUDA(cudaMemcpyAsync(supp.data(), d + osu, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i) supp[i] = (unsigned long long)db->plane_count[(hp[i] - db->planes) / db->words];
   // 2. ranks (support descending, ties by position) and the cost model
   std::vector<int> rank_item(n);
   std::iota(rank_item.begin(), rank_item.end(), 0);
@@ -2182,8 +2184,9 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   const size_t bpairs = sizeof(uint64_t) * (size_t)n * n, btri = sizeof(uint64_t) * std::max<int64_t>(ntri, 1);
   const size_t brm = sizeof(uint32_t) * (size_t)W * 32 * wr;
   const size_t ou = place(bu), opr = place(bpairs), otr = place(btri), orm = place(brm);
-  CS_TRY(ctx->scratch_get(11, off, &blob));  // grow (the support pass above is complete)
-  d = (char*)blob;
+  void* blob = nullptr;
+  CS_TRY(ctx->scratch_get(11, off, &blob));
+  char* d = (char*)blob;
   std::vector<const uint32_t*> rp(n);
   std::vector<int16_t> ri(SEL_MAXN, 0);
   for (int r = 0; r < n; ++r) rp[r] = hp[rank_item[r]], ri[r] = (int16_t)rank_item[r];
@@ -2191,7 +2194,6 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   const size_t hbytes = meta_end + bu;
   CS_TRY(ctx->pinned_get(hbytes, &hst));
   char* h = (char*)hst;
-  memcpy(h + op, hp.data(), bp);
   memcpy(h + ors, rp.data(), bp);
   memcpy(h + ori, ri.data(), sizeof(int16_t) * SEL_MAXN);
   if (!sorted.empty()) memcpy(h + ou, sorted.data(), sizeof(SelUnit) * sorted.size());
@@ -2201,11 +2203,6 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   CS_CUDA(cudaMemsetAsync(d + opr, 0, otr - opr + btri, ctx->stream));
   const int Rw = (int)round_up(n - 1, 8);  // Y row stride (ranks < rmax = n - 1)
   const size_t smem = sizeof(uint32_t) * (SEL_LCAP + (size_t)SEL_MAXB * Rw);
-  static bool attr = false;
-  if (!attr) {
-    CS_CUDA(cudaFuncSetAttribute((const void*)k_sel_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
   ctx->itemset_class = CS_ITEMSETS_SELECTOR;
   CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
   k_sel_rowmask<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((const uint32_t* const*)(d + ors), n, W, wr,
@@ -2337,12 +2334,7 @@ extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* ite
     // after the accumulator's columns), released in commit groups of cpc stages (a commit costs
     // short MMAs ~200 issue cycles, tools/microbench6.cu), and a raw ring of nr slots of
     // (the blocks' item slots + maxN) x 32 B.
-    static int smem_optin = 0;
-    if (!smem_optin) {
-      CS_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-      CS_CUDA(cudaFuncSetAttribute((const void*)k_itemsets_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_optin - 2048));
-    }
+    const int smem_optin = ctx->smem_optin;
     static const int tc_dbg = env_int("CS_TC_DEBUG", 0);  // diagnostic: skip work per role (wrong results)
 #ifdef CS_TC_PROFILE
     static const int tc_prof = env_int("CS_TC_PROF", 0);   // diagnostic: per-role wait cycles to stderr

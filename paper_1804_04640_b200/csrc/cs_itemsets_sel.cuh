@@ -13,7 +13,7 @@
 // pair plane with every item plane over all m records.  The host picks this class when its cost model says so
 // (cs_itemset_supports); results are identical.
 //
-//   k_sel_support   supports of the n items (popcount of the state-1 planes)
+//   (item supports = the state-1 plane counts recorded by cs_bitmap_build, k_plane_popc)
 //   k_sel_rowmask   record-major membership masks over the items in RANK order (rank 0 = most
 //                   frequent): rm[t][j] bit b = item of rank 32 j + b is in record t.  Warp per
 //                   32-record plane word: lane i loads the word of rank 32 j + i, 32 ballots
@@ -36,9 +36,10 @@ struct SelUnit {
   int64_t w0, w1;  // plane words [w0, w1), multiples of 32 x SEL_WARPS
 };
 
-__global__ void k_sel_support(const uint32_t* const* __restrict__ plane, int64_t words,
-                              unsigned long long* __restrict__ supp) {
-  const uint4* p = reinterpret_cast<const uint4*>(plane[blockIdx.y]);
+// record count of each of the bitmap index's planes (contiguous, `words` uint32 each): the
+// index's state counts, taken once when it is built
+__global__ void k_plane_popc(const uint32_t* __restrict__ planes, int64_t words, unsigned long long* __restrict__ cnt) {
+  const uint4* p = reinterpret_cast<const uint4*>(planes + (int64_t)blockIdx.y * words);
   const int64_t nv = words >> 2;
   uint32_t c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -47,7 +48,7 @@ __global__ void k_sel_support(const uint32_t* const* __restrict__ plane, int64_t
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(supp + blockIdx.y, (unsigned long long)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + blockIdx.y, (unsigned long long)c);
 }
 
 // rank_plane[k] = state-1 plane of the item of rank k (k < n); wr = words per record mask (1..8).
