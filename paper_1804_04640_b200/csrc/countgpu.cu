@@ -398,7 +398,43 @@ extern "C" int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_byt
 // ------------------------------------------------------------------------------------------
 // database
 
-static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, cs_db** out) {
+// 4-bit / 2-bit column copies for the bandwidth-bound histogram kernels, from db->arity
+static int db_alloc_copies(cs_db* db) {
+  cs_ctx* ctx = db->ctx;
+  const int n = db->n;
+  const int64_t m = db->m;
+  const std::vector<int32_t>& arities = db->arity;
+  // 4-bit copy for the bandwidth-bound histogram kernels when every arity fits a nibble
+  bool small = env_int("CS_NIBBLE", 1) != 0;
+  for (int i = 0; i < n && small; ++i) small = arities[i] <= 16;
+  if (small) {
+    db->ldn = round_up((m + 1) / 2, 256);
+    if (cudaMalloc(&db->nib, (size_t)n * db->ldn) != cudaSuccess) {
+      cudaGetLastError();  // not enough memory: the kernels read the uint8 columns instead
+      db->nib = nullptr;
+      db->ldn = 0;
+    } else {
+      CS_CUDA(cudaMemsetAsync(db->nib, 0, (size_t)n * db->ldn, ctx->stream));
+    }
+  }
+  // 2-bit copy when every arity <= 4 (the histogram kernels' smallest row footprint)
+  bool tiny = env_int("CS_CRUMB", 1) != 0;
+  for (int i = 0; i < n && tiny; ++i) tiny = arities[i] <= 4;
+  if (tiny) {
+    db->ldc = round_up((m + 3) / 4, 256);
+    if (cudaMalloc(&db->crumb, (size_t)n * db->ldc) != cudaSuccess) {
+      cudaGetLastError();
+      db->crumb = nullptr;
+      db->ldc = 0;
+    } else {
+      CS_CUDA(cudaMemsetAsync(db->crumb, 0, (size_t)n * db->ldc, ctx->stream));
+    }
+  }
+  return CS_OK;
+}
+
+static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, cs_db** out,
+                    bool copies = true) {
   if (!ctx || !out) return fail(CS_ERR_INVALID, "cs_db: NULL argument");
   if (n < 1 || m < 1)
     return fail(CS_ERR_INVALID, "database must have at least one variable and one row, got n=%d m=%lld",
@@ -432,32 +468,7 @@ static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, c
                           ctx->stream));
   // zero padding (and everything: generated DBs fill columns later)
   CS_CUDA(cudaMemsetAsync(db->cols, 0, (size_t)n * db->ld, ctx->stream));
-  // 4-bit copy for the bandwidth-bound histogram kernels when every arity fits a nibble
-  bool small = env_int("CS_NIBBLE", 1) != 0;
-  for (int i = 0; i < n && small; ++i) small = arities[i] <= 16;
-  if (small) {
-    db->ldn = round_up((m + 1) / 2, 256);
-    if (cudaMalloc(&db->nib, (size_t)n * db->ldn) != cudaSuccess) {
-      cudaGetLastError();  // not enough memory: the kernels read the uint8 columns instead
-      db->nib = nullptr;
-      db->ldn = 0;
-    } else {
-      CS_CUDA(cudaMemsetAsync(db->nib, 0, (size_t)n * db->ldn, ctx->stream));
-    }
-  }
-  // 2-bit copy when every arity <= 4 (the histogram kernels' smallest row footprint)
-  bool tiny = env_int("CS_CRUMB", 1) != 0;
-  for (int i = 0; i < n && tiny; ++i) tiny = arities[i] <= 4;
-  if (tiny) {
-    db->ldc = round_up((m + 3) / 4, 256);
-    if (cudaMalloc(&db->crumb, (size_t)n * db->ldc) != cudaSuccess) {
-      cudaGetLastError();
-      db->crumb = nullptr;
-      db->ldc = 0;
-    } else {
-      CS_CUDA(cudaMemsetAsync(db->crumb, 0, (size_t)n * db->ldc, ctx->stream));
-    }
-  }
+  if (copies) CS_TRY(db_alloc_copies(db));
   *out = db;
   return CS_OK;
 }
@@ -824,7 +835,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   // 5. database with placeholder arities (fixed below), then the parse
   std::vector<int32_t> ones(width, 1);
   cs_db* db = nullptr;
-  CS_TRY(db_alloc(ctx, (int32_t)width, nrec, ones.data(), &db));
+  CS_TRY(db_alloc(ctx, (int32_t)width, nrec, ones.data(), &db, /*copies=*/false));
   int rc = CS_OK;
   auto drop = [&](int code) {
     cs_db_destroy(db);
@@ -933,18 +944,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   }
   db->arity = ar;
   CS_CUDA(cudaMemcpyAsync(db->d_arity, ar.data(), sizeof(int32_t) * width, cudaMemcpyHostToDevice, st));
-  if (db->crumb && *std::max_element(ar.begin(), ar.end()) > 4) {
-    CS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(db->crumb);
-    db->crumb = nullptr;
-    db->ldc = 0;
-  }
-  if (db->nib && *std::max_element(ar.begin(), ar.end()) > 16) {
-    CS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(db->nib);
-    db->nib = nullptr;
-    db->ldn = 0;
-  }
+  if ((rc = db_alloc_copies(db))) return drop(rc);  // now that the arities are known
   if ((rc = db_pack(db, 0, db->n))) return drop(rc);
   CS_CUDA(cudaStreamSynchronize(st));
   *out = db;

@@ -120,7 +120,7 @@ __device__ __forceinline__ int64_t sel_triple_index(int n, int a, int b, int c) 
   return c3(n) - c3(n - a) + c2(n - a - 1) - c2(n - b) + (c - b - 1);
 }
 
-constexpr int SEL_LCAP = 2048;           // compacted records per round
+constexpr int SEL_LCAP = 3072;           // compacted records per round (2 CTAs x ~89 KB SMEM per SM)
 constexpr int SEL_MAXB = SEL_LCAP / 32;  // 32-record batches per round
 
 // A2 of k_sel_gram for units whose masks below rank r span NWR words: warp per 32-record

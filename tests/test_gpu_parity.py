@@ -716,3 +716,43 @@ def test_pipelined_instance_sharded_single_rank(ctx):
     plan.execute(loglik=ll0, mi=mi0)
     assert np.allclose(ll.cpu().numpy(), ll0, rtol=1e-12, atol=1e-9)
     assert np.allclose(mi.cpu().numpy(), mi0, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", ["one_row", "one_variable", "constant_columns", "arity_256",
+                                   "ragged_m_2bit", "ragged_m_4bit", "ragged_m_u8"])
+def test_edge_databases(ctx, shape):
+    """Degenerate databases through the counting plan vs the radix restatement (tables bit-exact,
+    LL to 1e-9): a single record, a single variable (target-only queries), arity-1 (constant)
+    variables, the maximum arity 256, and row counts that are not multiples of the 16/32/64-row
+    vectors of the uint8 / 4-bit / 2-bit layouts.  Also an empty batch."""
+    rng = np.random.default_rng(sum(shape.encode()))
+    if shape == "one_row":
+        ar = np.array([3, 2, 4, 2]); m = 1
+    elif shape == "one_variable":
+        ar = np.array([5]); m = 1_001
+    elif shape == "constant_columns":
+        ar = np.array([1, 3, 1, 2, 4]); m = 5_003
+    elif shape == "arity_256":
+        ar = np.array([256, 2, 3, 256]); m = 70_001
+    elif shape == "ragged_m_2bit":
+        ar = np.array([2, 3, 4, 4, 2, 3]); m = 100_003
+    elif shape == "ragged_m_4bit":
+        ar = np.array([2, 7, 16, 5, 3, 9]); m = 100_007
+    else:
+        ar = np.array([2, 17, 30, 5, 3, 9]); m = 100_011
+    u8 = np.stack([rng.integers(0, a, size=m) for a in ar]).astype(np.uint8)
+    gdb = GpuDatabase.from_columns(ctx, u8, ar)
+    n = len(ar)
+    qs = [(v,) for v in range(n)]
+    if n > 1:
+        qs += [tuple(int(x) for x in rng.permutation(n)[:k]) for k in range(2, min(n, 4) + 1) for _ in range(3)]
+    plan = QueryPlan(gdb, qs, cs._native.CS_WANT_TABLES)
+    tabs = np.zeros(plan.total_cells, dtype=np.uint32)
+    ll = np.zeros(plan.nq)
+    plan.execute(tables=tabs, loglik=ll)
+    otabs, _, oll, _ = O.radix_tables(u8, ar, qs)
+    assert np.array_equal(tabs, otabs)
+    assert np.allclose(ll, oll, rtol=1e-9, atol=1e-9)
+    empty = QueryPlan(gdb, [], cs._native.CS_WANT_TABLES)
+    assert empty.nq == 0 and empty.total_cells == 0
+    empty.execute(tables=np.zeros(1, dtype=np.uint32), loglik=np.zeros(1))
