@@ -2136,6 +2136,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   // cost model: k_sel_gram issues ~r^2/64 popcounts per selected record of rank r (8 x 4
   // register blocks over 32-record batches), plus the record gathers
   std::vector<double> cost(n, 0.0);
+  std::vector<char> dmode(n, 0);
   double total = 0.0, gathered = 0.0;
   for (int r = 1; r < n; ++r) {
     const double sr = (double)supp[rank_item[r]];
@@ -2144,7 +2145,11 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
     for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
     // warp instructions: Gram 3 x 32 popc-steps per block per 32-record batch, the batch
     // transposes ~30 per mask word per batch, the selector-plane scan ~1.25 per word
-    cost[r] = sr * (0.094 * nblk + (r + 31) / 32 + 1.0) + 1.25 * (double)W;
+    const double compact = sr * (0.094 * nblk + (r + 31) / 32 + 1.0) + 1.25 * (double)W;
+    // dense selectors: every plane word is a batch (Y = P_y & P_s), no list / gather / transpose
+    const double direct = (double)W * (3.0 * nblk + 0.19 * r + 1.0);
+    dmode[r] = direct < compact;
+    cost[r] = std::min(compact, direct);
     total += cost[r];
     gathered += sr;
   }
@@ -2156,7 +2161,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
   // 3. record-major rank masks
   const int wr = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
   // units: (rank, word range) with ~equal cost, ranges in multiples of 512 words (16 warps x 32)
-  const double target = std::max(1.0, total / (ctx->num_sms * 48.0));
+  const double target = std::max(1.0, total / (ctx->num_sms * (double)env_int("CS_SEL_UNITS", 48)));
   std::vector<SelUnit> units;
   std::vector<double> ucost;
   for (int r = 1; r < n; ++r) {
@@ -2166,11 +2171,11 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
     for (int y = 0; y < nby && 2 * y < nbz; ++y) nblk += nbz - 2 * y;
     const int nsplit = (nblk + SEL_THREADS - 1) / SEL_THREADS;  // block ranges of <= SEL_THREADS
     int64_t chunks = std::max<int64_t>(1, (int64_t)std::ceil(cost[r] / target / nsplit));
-    const int64_t per = round_up((W + chunks - 1) / chunks, 32 * SEL_WARPS);
+    const int64_t per = round_up((W + chunks - 1) / chunks, 128 * SEL_WARPS);  // A1 chunk stride
     for (int sp = 0; sp < nsplit; ++sp) {
       const int b0 = (int)((int64_t)nblk * sp / nsplit), b1 = (int)((int64_t)nblk * (sp + 1) / nsplit);
       for (int64_t w0 = 0; w0 < W; w0 += per) {
-        units.push_back(SelUnit{r, (int16_t)b0, (int16_t)b1, w0, std::min(W, w0 + per)});
+        units.push_back(SelUnit{r | (dmode[r] ? 1 << 30 : 0), (int16_t)b0, (int16_t)b1, w0, std::min(W, w0 + per)});
         ucost.push_back(cost[r] / nsplit * (double)(std::min(W, w0 + per) - w0) / (double)W + 2.0 * (b1 - b0));
       }
     }
@@ -2212,7 +2217,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
     k_sel_gram<<<2 * ctx->num_sms, SEL_THREADS, smem, ctx->stream>>>(
         (const uint32_t* const*)(d + ors), (const uint32_t*)(d + orm), wr, (const int16_t*)(d + ori), n,
         (const SelUnit*)(d + ou), (int)sorted.size(), (int*)(d + ohd), Rw, (unsigned long long*)(d + opr),
-        (unsigned long long*)(d + otr));
+        (unsigned long long*)(d + otr), env_int("CS_SEL_DEBUG", 0));  // diagnostic: skip phases (wrong results)
     ctx->launches++;
   }
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

@@ -132,6 +132,9 @@ __device__ __forceinline__ void sel_batches(const uint32_t* __restrict__ rm, int
                                             int lane) {
   for (int b = warp; b < nbatch; b += SEL_WARPS) {
     const int i = 32 * b + lane;
+    // the warp's next batch: pull its records' mask rows into L2 now (no registers held)
+    const int i2 = i + 32 * SEL_WARPS;
+    if (i2 < cnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(rm + (int64_t)list[i2] * wr));
     uint32_t mw[NWR];
 #pragma unroll
     for (int j = 0; j < NWR; ++j) mw[j] = 0u;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
     const uint32_t* const* __restrict__ rank_plane, const uint32_t* __restrict__ rm, int wr,
     const int16_t* __restrict__ rank_item, int n, const SelUnit* __restrict__ units, int nunits,
     int* __restrict__ head, int R, unsigned long long* __restrict__ pairs,
-    unsigned long long* __restrict__ triples) {
+    unsigned long long* __restrict__ triples, int dbg) {
   extern __shared__ __align__(16) uint32_t sel_smem[];
   uint32_t* list = sel_smem;
   uint32_t* Y = sel_smem + SEL_LCAP;
@@ -201,7 +204,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
     const int ui = s_unit;
     if (ui >= nunits) return;
     const SelUnit u = units[ui];
-    const int r = u.r;
+    const int r = u.r & 0xffff;
+    const bool direct = (u.r >> 30) & 1;  // dense selector: batches = plane words, no compaction
     // Gram blocks: 8 ranks (y) x 4 ranks (z), only blocks holding some y <= z (bz >= 2 by)
     const int nby = (r + 7) >> 3, nbz = (r + 3) >> 2;
     // this unit's Gram blocks: [blk0, blk1) of the rank's 8 x 4 blocks holding some y <= z
@@ -231,21 +235,49 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
     const int nwr = (r + 31) >> 5;
     const uint32_t lastmask = (r & 31) ? (1u << (r & 31)) - 1 : 0xffffffffu;
     const uint32_t* sp = rank_plane[r];
-    int64_t wnext = u.w0 + 32 * warp;
+    int64_t wnext = u.w0 + 128 * warp;
+    int64_t wdir = u.w0;  // direct mode: next plane word
     for (;;) {
+      bool done;
+      int nbatch;
+      if (direct) {
+        // batch b = plane word wdir + b: Y[b][y] = P_y & P_s (records of the word holding both);
+        // ranks [r, 8 nby) are zeroed for the last Gram block row
+        nbatch = (int)(u.w1 - wdir < SEL_MAXB ? u.w1 - wdir : SEL_MAXB);
+        const int ny = min(R, 8 * nby);
+        for (int i = threadIdx.x; i < ny * nbatch; i += SEL_THREADS) {
+          const int y = i / nbatch, b = i - y * nbatch;
+          Y[b * R + y] = y < r ? __ldg(rank_plane[y] + wdir + b) & __ldg(sp + wdir + b) : 0u;
+        }
+        wdir += nbatch;
+        done = wdir >= u.w1;
+        __syncthreads();
+      } else {
       if (threadIdx.x == 0) {
         s_cnt = 0;
         s_end = SEL_LCAP;
       }
       __syncthreads();
       // A1: append selected records until the range ends or a chunk does not fit
-      // the next chunk's selector word is loaded while this one is compacted
-      uint32_t xn = wnext < u.w1 ? sp[wnext + lane] : 0u;
+      // A1 chunks: 4 words (128 records) per lane, 128 words per warp; the next two chunks'
+      // selector words are in flight while one is compacted (the scan is latency-bound: one
+      // 128-B request per warp kept only ~0.6 TB/s of plane reads in flight)
+      auto load4 = [&](int64_t w) -> uint4 {
+        if (w + 4 <= u.w1) return __ldg(reinterpret_cast<const uint4*>(sp + w));
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (w < u.w1) v.x = sp[w];
+        if (w + 1 < u.w1) v.y = sp[w + 1];
+        if (w + 2 < u.w1) v.z = sp[w + 2];
+        return v;
+      };
+      const int64_t stride = 128 * SEL_WARPS;
+      uint4 xa = load4(wnext + 4 * lane), xb = load4(wnext + stride + 4 * lane);
       while (wnext < u.w1) {
-        uint32_t x = xn;
-        const int64_t wn2 = wnext + 32 * SEL_WARPS;
-        xn = wn2 < u.w1 ? sp[wn2 + lane] : 0u;
-        const int c = __popc(x);
+        const uint4 xc = xa;
+        xa = xb;
+        xb = load4(wnext + 2 * stride + 4 * lane);
+        uint32_t xs[4] = {xc.x, xc.y, xc.z, xc.w};
+        const int c = __popc(xs[0]) + __popc(xs[1]) + __popc(xs[2]) + __popc(xs[3]);
         int pre = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -260,23 +292,28 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base + total > SEL_LCAP) {
           if (lane == 0) atomicMin(&s_end, base);
+          // the two loads in flight are dropped; the next round reloads from wnext
           break;
         }
         int pos = base + pre - c;
-        const uint32_t rec0 = (uint32_t)((wnext + lane) * 32);
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1;
-          list[pos++] = rec0 + b;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t x = xs[j];
+          const uint32_t rec0 = (uint32_t)((wnext + 4 * lane + j) * 32);
+          while (x) {
+            const int bit = __ffs(x) - 1;
+            x &= x - 1;
+            list[pos++] = rec0 + bit;
+          }
         }
-        wnext += 32 * SEL_WARPS;
+        wnext += stride;
       }
-      const bool done = __syncthreads_and(wnext >= u.w1);
+      done = __syncthreads_and(wnext >= u.w1);
       const int cnt = min(s_cnt, s_end);
-      const int nbatch = (cnt + 31) >> 5;
+      nbatch = (cnt + 31) >> 5;
       // A2: batch transposes (masks below rank r only; y in [r, R) comes out zero), unrolled
       // for the unit's mask-word count
-      switch (nwr) {
+      if (!(dbg & 2)) switch (nwr) {
         case 1: sel_batches<1>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
         case 2: sel_batches<2>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
         case 3: sel_batches<3>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
@@ -287,8 +324,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
         default: sel_batches<8>(rm, wr, list, cnt, nbatch, lastmask, R, Y, warp, lane); break;
       }
       __syncthreads();
+      }  // compacted mode
       // B: Gram of the batches
-      if (by >= 0) {
+      if (by >= 0 && !(dbg & 1)) {
         for (int b = grp; b < nbatch; b += ngrp) {
           const uint4* yp = reinterpret_cast<const uint4*>(Y + b * R + 8 * by);
           const uint4 y0 = yp[0], y1 = yp[1], z0 = *reinterpret_cast<const uint4*>(Y + b * R + 4 * bz);
@@ -304,7 +342,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_sel_gram(
       if (done) break;
     }
     // flush: y <= z < r
-    if (by >= 0) {
+    if (by >= 0 && !(dbg & 4)) {
       const int s = s_item[r];
 #pragma unroll
       for (int a = 0; a < 8; ++a)
