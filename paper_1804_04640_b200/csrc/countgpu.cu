@@ -1228,8 +1228,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   }
   const double trp = now_ms();
   // serial pass: table offsets, hash-class descriptors, generic-class variable lists
+  int64_t nkind[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // queries per class: later passes skip empty ones
   for (int q = 0; q < nq; ++q) {
     QDesc& d = p->hq[q];
+    nkind[d.kind & 7]++;
     const int b = var_off[q], k = var_off[q + 1] - b;
     d.table_off = total;
     if (d.kind == 3) {
@@ -1398,7 +1400,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // global class: query-major (all segments of a query back to back, queries LPT by total
   // cost) so concurrently running CTAs share one L2-resident table -- RED.ADD throughput
   // collapses when they spray many >SMEM tables at once
-  {
+  if (nkind[1]) {
     std::map<int, double> qcost;
     std::vector<int> gq;
     for (size_t i = 0; i < items.size(); ++i)
@@ -1417,7 +1419,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // partition class (kind 4): descriptors in wave order (waves grouped by digit count), count
   // items per (query, 32K-cell group, chunk range)
   std::vector<RItem> ritems;
-  {
+  if (nkind[4]) {
     std::vector<int> rq;
     for (int q = 0; q < nq; ++q)
       if (p->hq[q].kind == 4) rq.push_back(q);
