@@ -170,6 +170,7 @@ struct cs_db {
   uint8_t* nib = nullptr;  // 4-bit copy (all arities <= 16), ldn bytes per column
   int64_t ldn = 0;
   uint8_t* crumb = nullptr;  // 2-bit copy (all arities <= 4), ldc bytes per column
+  bool pooled = false;       // buffers from the stream-ordered pool (text ingest)
   int64_t ldc = 0;
   int32_t* d_arity = nullptr;
   std::vector<int32_t> arity;
@@ -398,6 +399,17 @@ extern "C" int cs_ctx_info(cs_ctx* ctx, int32_t* num_sms, int32_t* hist_smem_byt
 // ------------------------------------------------------------------------------------------
 // database
 
+// Database buffers: cudaMalloc, or (databases parsed from text) the device's stream-ordered
+// pool, whose freed blocks are kept for the next load instead of a cudaMalloc / cudaFree pair
+static cudaError_t db_malloc(cs_db* db, void** p, size_t bytes) {
+  return db->pooled ? cudaMallocAsync(p, bytes, db->ctx->stream) : cudaMalloc(p, bytes);
+}
+static void db_free(cs_db* db, void* p) {
+  if (!p) return;
+  if (db->pooled) cudaFreeAsync(p, db->ctx->stream);
+  else cudaFree(p);
+}
+
 // 4-bit / 2-bit column copies for the bandwidth-bound histogram kernels, from db->arity
 static int db_alloc_copies(cs_db* db) {
   cs_ctx* ctx = db->ctx;
@@ -409,7 +421,7 @@ static int db_alloc_copies(cs_db* db) {
   for (int i = 0; i < n && small; ++i) small = arities[i] <= 16;
   if (small) {
     db->ldn = round_up((m + 1) / 2, 256);
-    if (cudaMalloc(&db->nib, (size_t)n * db->ldn) != cudaSuccess) {
+    if (db_malloc(db, (void**)&db->nib, (size_t)n * db->ldn) != cudaSuccess) {
       cudaGetLastError();  // not enough memory: the kernels read the uint8 columns instead
       db->nib = nullptr;
       db->ldn = 0;
@@ -422,7 +434,7 @@ static int db_alloc_copies(cs_db* db) {
   for (int i = 0; i < n && tiny; ++i) tiny = arities[i] <= 4;
   if (tiny) {
     db->ldc = round_up((m + 3) / 4, 256);
-    if (cudaMalloc(&db->crumb, (size_t)n * db->ldc) != cudaSuccess) {
+    if (db_malloc(db, (void**)&db->crumb, (size_t)n * db->ldc) != cudaSuccess) {
       cudaGetLastError();
       db->crumb = nullptr;
       db->ldc = 0;
@@ -434,7 +446,7 @@ static int db_alloc_copies(cs_db* db) {
 }
 
 static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, cs_db** out,
-                    bool copies = true) {
+                    bool copies = true, bool pooled = false) {
   if (!ctx || !out) return fail(CS_ERR_INVALID, "cs_db: NULL argument");
   if (n < 1 || m < 1)
     return fail(CS_ERR_INVALID, "database must have at least one variable and one row, got n=%d m=%lld",
@@ -456,14 +468,15 @@ static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, c
   db->ld = round_up(m, 256);
   db->arity.assign(arities, arities + n);
   db->plane_off.assign(n, -1);
-  cudaError_t e = cudaMalloc(&db->cols, (size_t)n * db->ld);
+  db->pooled = pooled;
+  cudaError_t e = db_malloc(db, (void**)&db->cols, (size_t)n * db->ld);
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete db;
     return fail(CS_ERR_OOM, "cs_db: cannot allocate %lld bytes of columns: %s",
                 (long long)n * db->ld, cudaGetErrorString(e));
   }
-  CS_CUDA(cudaMalloc(&db->d_arity, sizeof(int32_t) * n));
+  CS_CUDA(db_malloc(db, (void**)&db->d_arity, sizeof(int32_t) * n));
   CS_CUDA(cudaMemcpyAsync(db->d_arity, arities, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
                           ctx->stream));
   // zero padding (and everything: generated DBs fill columns later)
@@ -590,10 +603,11 @@ extern "C" int cs_db_destroy(cs_db* db) {
   if (!db) return CS_OK;
   cudaSetDevice(db->ctx->device);
   cudaStreamSynchronize(db->ctx->stream);
-  if (db->cols) cudaFree(db->cols);
-  if (db->nib) cudaFree(db->nib);
-  if (db->crumb) cudaFree(db->crumb);
-  if (db->d_arity) cudaFree(db->d_arity);
+  db_free(db, db->cols);
+  db_free(db, db->nib);
+  db_free(db, db->crumb);
+  db_free(db, db->d_arity);
+  if (db->pooled) cudaStreamSynchronize(db->ctx->stream);
   if (db->planes) cudaFree(db->planes);
   delete db;
   return CS_OK;
@@ -835,7 +849,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   // 5. database with placeholder arities (fixed below), then the parse
   std::vector<int32_t> ones(width, 1);
   cs_db* db = nullptr;
-  CS_TRY(db_alloc(ctx, (int32_t)width, nrec, ones.data(), &db, /*copies=*/false));
+  CS_TRY(db_alloc(ctx, (int32_t)width, nrec, ones.data(), &db, /*copies=*/false, /*pooled=*/true));
   int rc = CS_OK;
   auto drop = [&](int code) {
     cs_db_destroy(db);
