@@ -134,9 +134,18 @@ struct cs_ctx {
   // grow-only pinned staging
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // pipelined cs_query_batch: chunk j plans into scratch bank j&1 while chunk j-1's kernels run;
+  // bank 1 has its own device scratch slots and pinned staging, each bank's staging upload is
+  // guarded by an event instead of a stream sync, and per-chunk output syncs are deferred
+  int bank = 0;
+  bool pipe = false;
+  void* pinned1 = nullptr;
+  size_t pinned1_bytes = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  bool stage_ev_valid[2] = {false, false};
 
   int scratch_get(int slot, size_t bytes, void** out) {
-    auto& s = scratch[slot];
+    auto& s = scratch[slot + 1000 * bank];
     if (s.second < bytes) {
       if (s.first) cudaFree(s.first);
       s.first = nullptr;
@@ -149,15 +158,17 @@ struct cs_ctx {
     return CS_OK;
   }
   int pinned_get(size_t bytes, void** out) {
-    if (pinned_bytes < bytes) {
-      if (pinned) cudaFreeHost(pinned);
-      pinned = nullptr;
-      pinned_bytes = 0;
+    void*& pb = bank ? pinned1 : pinned;
+    size_t& pn = bank ? pinned1_bytes : pinned_bytes;
+    if (pn < bytes) {
+      if (pb) cudaFreeHost(pb);
+      pb = nullptr;
+      pn = 0;
       size_t want = std::max<size_t>(bytes, 1 << 20);
-      CS_CUDA(cudaHostAlloc(&pinned, want, cudaHostAllocDefault));
-      pinned_bytes = want;
+      CS_CUDA(cudaHostAlloc(&pb, want, cudaHostAllocDefault));
+      pn = want;
     }
-    *out = pinned;
+    *out = pb;
     return CS_OK;
   }
 };
@@ -337,6 +348,9 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
   for (auto& kv : ctx->scratch)
     if (kv.second.first) cudaFree(kv.second.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->pinned1) cudaFreeHost(ctx->pinned1);
+  for (auto& e : ctx->stage_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1545,7 +1559,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   }
   void* stage = nullptr;
   CS_TRY(ctx->pinned_get(off, &stage));
-  CS_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer may be in flight
+  if (ctx->pipe) {
+    // only this bank's previous upload can still be reading its staging buffer
+    if (ctx->stage_ev_valid[ctx->bank]) CS_CUDA(cudaEventSynchronize(ctx->stage_ev[ctx->bank]));
+  } else {
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer may be in flight
+  }
   char* hs = (char*)stage;
   memcpy(hs + oq, p->hq.data(), sizeof(QDesc) * nq);
   memcpy(hs + oi, sorted.data(), sizeof(WItem) * sorted.size());
@@ -1558,6 +1577,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   CS_CUDA(cudaMemcpyAsync(dblob, hs, oh, cudaMemcpyHostToDevice, ctx->stream));
   if (!p->rdesc.empty())
     CS_CUDA(cudaMemcpyAsync(dblob + ord, hs + ord, orh - ord, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->pipe) {
+    auto& ev = ctx->stage_ev[ctx->bank];
+    if (!ev) CS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CS_CUDA(cudaEventRecord(ev, ctx->stream));
+    ctx->stage_ev_valid[ctx->bank] = true;
+  }
   p->d_q = (QDesc*)(dblob + oq);
   p->d_items = (WItem*)(dblob + oi);
   p->d_score_list = (int32_t*)(dblob + os);
@@ -1712,7 +1737,7 @@ static int finish_outputs(cs_ctx* ctx, OutBuf* obs, int nob) {
       any_host = true;
     }
   }
-  if (any_host) CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (any_host && !ctx->pipe) CS_CUDA(cudaStreamSynchronize(ctx->stream));
   return CS_OK;
 }
 
@@ -2027,11 +2052,65 @@ extern "C" int cs_family_scores(cs_ctx* ctx, int64_t nfam, const double* nlogn, 
   return finish_outputs(ctx, obs, 2);
 }
 
+static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
+                                 uint32_t flags, uint32_t* tables, double* loglik, double* mi, int64_t* nnz,
+                                 int nchunks, bool trace) {
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (!var_off || !vars) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
+  nchunks = std::min(nchunks, 8);
+  struct Restore {  // leave the context in single-bank, synchronous mode on every exit
+    cs_ctx* c;
+    ~Restore() {
+      c->bank = 0;
+      c->pipe = false;
+      cudaStreamSynchronize(c->stream);
+    }
+  } restore{ctx};
+  ctx->pipe = true;
+  const int64_t denom = (1LL << nchunks) - 1;
+  int64_t cell_off = 0;
+  int32_t q0 = 0;
+  double tplan = 0.0;
+  for (int j = 0; j < nchunks; ++j) {
+    const int32_t q1 = j == nchunks - 1 ? nq : (int32_t)((int64_t)nq * ((1LL << (j + 1)) - 1) / denom);
+    if (q1 <= q0) continue;
+    ctx->bank = j & 1;
+    cs_plan* p = nullptr;
+    const double t0 = trace ? now_ms() : 0.0;
+    CS_TRY(plan_build(db, q1 - q0, var_off + q0, vars, flags, &p, /*transient=*/true));
+    if (trace) tplan += now_ms() - t0;
+    const int rc = cs_plan_execute(p, tables ? tables + cell_off : nullptr, loglik ? loglik + q0 : nullptr,
+                                   mi ? mi + q0 : nullptr, nnz ? nnz + q0 : nullptr);
+    cell_off += p->total_cells;
+    cs_plan_destroy(p);
+    if (rc != CS_OK) return rc;
+    q0 = q1;
+  }
+  if (trace) fprintf(stderr, "cs_query_batch: %d chunks, plan %.3f ms (host, overlapped after the first)\n",
+                     nchunks, tplan);
+  ctx->pipe = false;
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
 extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                               uint32_t flags, uint32_t* tables, double* loglik, double* mi,
                               int64_t* nnz) {
   cs_plan* p = nullptr;
   const bool trace = env_int("CS_TRACE", 0) != 0;
+  // big batches: plan chunk j+1 on the host while chunk j's kernels run (chunk sizes double,
+  // so each chunk's execution covers the next chunk's planning; only the first plan is exposed).
+  // Chunks below ~3K queries lose more to K1 launch tails than planning costs (cfg2 e2e, 10K
+  // queries: 1 chunk 4.08 ms, 2 chunks 3.90, 3 chunks 4.13; cfg3, 289K: 30.7 -> 25.1 ms at 4)
+  int nchunks = env_int("CS_QB_CHUNKS", 0);
+  if (nchunks <= 0) {
+    const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 3000), 1);
+    nchunks = 1;
+    while (nchunks < 4 && (int64_t)nq / ((1LL << (nchunks + 1)) - 1) >= min_chunk) ++nchunks;
+  }
+  if (db && nchunks > 1 && nq >= 2) return query_batch_pipelined(db, nq, var_off, vars, flags, tables,
+                                                                         loglik, mi, nnz, nchunks, trace);
   const double t0 = trace ? now_ms() : 0.0;
   CS_TRY(plan_build(db, nq, var_off, vars, flags, &p, /*transient=*/true));
   const double t1 = trace ? now_ms() : 0.0;

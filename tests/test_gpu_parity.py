@@ -756,3 +756,56 @@ def test_edge_databases(ctx, shape):
     empty = QueryPlan(gdb, [], cs._native.CS_WANT_TABLES)
     assert empty.nq == 0 and empty.total_cells == 0
     empty.execute(tables=np.zeros(1, dtype=np.uint32), loglik=np.zeros(1))
+
+
+@pytest.mark.parametrize("outputs", ["pageable", "pinned", "device"])
+def test_query_batch_pipelined_chunks(ctx, outputs, monkeypatch):
+    """cs_query_batch over >= CS_QB_PIPE_MIN queries plans chunk j+1 while chunk j runs (two
+    scratch banks, deferred syncs): tables / LL / MI / nnz bit-identical to the one-plan path
+    and to the oracle's radix restatement."""
+    import torch
+
+    rng = np.random.default_rng(1804)
+    n, m = 24, 150_000
+    arities = rng.integers(2, 6, size=n).astype(np.int32)
+    cols = np.stack([rng.integers(0, a, size=m) for a in arities]).astype(np.uint8)
+    queries = [tuple(int(v) for v in rng.choice(n, size=int(rng.integers(1, 5)), replace=False))
+               for _ in range(5000)]
+    gdb = GpuDatabase.from_columns(ctx, cols, arities)
+    from paper_1804_04640_b200.engine import encode_queries
+
+    off, flat = encode_queries(queries)
+    cells = np.array([int(np.prod([int(arities[v]) for v in q])) for q in queries], dtype=np.int64)
+    total = int(cells.sum())
+    flags = cs._native.CS_WANT_TABLES
+
+    def run(chunks):
+        if chunks:
+            monkeypatch.setenv("CS_QB_CHUNKS", str(chunks))
+        if outputs == "device":
+            mk = lambda k, dt: torch.zeros(k, dtype=dt, device="cuda")  # noqa: E731
+        elif outputs == "pinned":
+            mk = lambda k, dt: torch.zeros(k, dtype=dt).pin_memory()  # noqa: E731
+        else:
+            mk = lambda k, dt: torch.zeros(k, dtype=dt)  # noqa: E731
+        t, ll, mi, nz = (mk(total, torch.int32), mk(len(queries), torch.float64),
+                         mk(len(queries), torch.float64), mk(len(queries), torch.int64))
+        gdb.query_batch(off, flat, flags, tables=t, loglik=ll, mi=mi, nnz=nz)
+        torch.cuda.synchronize()
+        return [x.cpu().numpy() for x in (t, ll, mi, nz)]
+
+    one = run(1)
+    for chunks in (2, 3, 5):
+        got = run(chunks)
+        # counts bit-exact; the fp64 scores' summation order follows each chunk's row segmentation
+        assert np.array_equal(one[0], got[0]) and np.array_equal(one[3], got[3]), chunks
+        assert all(rel_close(a, b, 1e-12) for a, b in zip(one[1], got[1])), chunks
+        assert all(rel_close(a, b, 1e-12) or abs(a - b) < 1e-12 for a, b in zip(one[2], got[2])), chunks
+    monkeypatch.delenv("CS_QB_CHUNKS")
+    monkeypatch.setenv("CS_QB_MIN_CHUNK", "700")  # automatic split: 5000 queries -> 3 chunks
+    auto = run(0)
+    assert np.array_equal(one[0], auto[0]) and np.array_equal(one[3], auto[3])
+    otabs, _, oll, onnz = O.radix_tables(cols, arities, queries)
+    assert np.array_equal(one[0].view(np.uint32), otabs)
+    assert np.array_equal(one[3], onnz)
+    assert all(rel_close(a, b, 1e-9) for a, b in zip(one[1], oll))
