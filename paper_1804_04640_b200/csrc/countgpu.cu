@@ -2059,6 +2059,12 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
   CS_CUDA(cudaSetDevice(ctx->device));
   if (!var_off || !vars) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
   nchunks = std::min(nchunks, 8);
+  // chunk j holds a growth^j share of the batch (growth 4: 1/5 + 4/5, 1/21 + 4/21 + 16/21, ...)
+  const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 4), 1), 8);
+  std::vector<int64_t> gp(nchunks + 1, 1);
+  for (int j = 1; j <= nchunks; ++j) gp[j] = gp[j - 1] * growth;
+  int64_t wsum = 0;
+  for (int j = 0; j < nchunks; ++j) wsum += gp[j];
   struct Restore {  // leave the context in single-bank, synchronous mode on every exit
     cs_ctx* c;
     ~Restore() {
@@ -2068,12 +2074,12 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
     }
   } restore{ctx};
   ctx->pipe = true;
-  const int64_t denom = (1LL << nchunks) - 1;
-  int64_t cell_off = 0;
+  int64_t cell_off = 0, wcum = 0;
   int32_t q0 = 0;
   double tplan = 0.0;
   for (int j = 0; j < nchunks; ++j) {
-    const int32_t q1 = j == nchunks - 1 ? nq : (int32_t)((int64_t)nq * ((1LL << (j + 1)) - 1) / denom);
+    wcum += gp[j];
+    const int32_t q1 = j == nchunks - 1 ? nq : (int32_t)((int64_t)nq * wcum / wsum);
     if (q1 <= q0) continue;
     ctx->bank = j & 1;
     cs_plan* p = nullptr;
@@ -2101,13 +2107,22 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
   const bool trace = env_int("CS_TRACE", 0) != 0;
   // big batches: plan chunk j+1 on the host while chunk j's kernels run (chunk sizes double,
   // so each chunk's execution covers the next chunk's planning; only the first plan is exposed).
-  // Chunks below ~3K queries lose more to K1 launch tails than planning costs (cfg2 e2e, 10K
-  // queries: 1 chunk 4.08 ms, 2 chunks 3.90, 3 chunks 4.13; cfg3, 289K: 30.7 -> 25.1 ms at 4)
+  // Chunk j holds a CS_QB_GROWTH^j share; a first chunk below ~2K queries loses more to K1
+  // launch tails than its planning costs (cfg2 e2e, 10K queries: one plan 4.08 ms; 2 chunks at
+  // growth 2/3/4: 3.89/3.85/3.81; 3 chunks at growth 2/3/4: 4.13/4.01/3.93; cfg3, 289K
+  // queries: 30.7 -> 24.5-24.7 ms for 3-5 chunks at growth 2-3)
   int nchunks = env_int("CS_QB_CHUNKS", 0);
   if (nchunks <= 0) {
-    const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 3000), 1);
+    const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 2000), 1);
+    const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 4), 1), 8);
+    int64_t w = 1, wsum = 1;
     nchunks = 1;
-    while (nchunks < 4 && (int64_t)nq / ((1LL << (nchunks + 1)) - 1) >= min_chunk) ++nchunks;
+    while (nchunks < 4) {
+      w *= growth;
+      if ((int64_t)nq / (wsum + w) < min_chunk) break;
+      wsum += w;
+      ++nchunks;
+    }
   }
   if (db && nchunks > 1 && nq >= 2) return query_batch_pipelined(db, nq, var_off, vars, flags, tables,
                                                                          loglik, mi, nnz, nchunks, trace);

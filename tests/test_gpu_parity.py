@@ -795,14 +795,16 @@ def test_query_batch_pipelined_chunks(ctx, outputs, monkeypatch):
         return [x.cpu().numpy() for x in (t, ll, mi, nz)]
 
     one = run(1)
-    for chunks in (2, 3, 5):
+    for chunks, growth in ((2, 4), (3, 2), (5, 3)):
+        monkeypatch.setenv("CS_QB_GROWTH", str(growth))
         got = run(chunks)
         # counts bit-exact; the fp64 scores' summation order follows each chunk's row segmentation
         assert np.array_equal(one[0], got[0]) and np.array_equal(one[3], got[3]), chunks
         assert all(rel_close(a, b, 1e-12) for a, b in zip(one[1], got[1])), chunks
         assert all(rel_close(a, b, 1e-12) or abs(a - b) < 1e-12 for a, b in zip(one[2], got[2])), chunks
     monkeypatch.delenv("CS_QB_CHUNKS")
-    monkeypatch.setenv("CS_QB_MIN_CHUNK", "700")  # automatic split: 5000 queries -> 3 chunks
+    monkeypatch.delenv("CS_QB_GROWTH")
+    monkeypatch.setenv("CS_QB_MIN_CHUNK", "200")  # automatic split: 5000 queries -> 3 chunks
     auto = run(0)
     assert np.array_equal(one[0], auto[0]) and np.array_equal(one[3], auto[3])
     otabs, _, oll, onnz = O.radix_tables(cols, arities, queries)
