@@ -26,7 +26,7 @@ import numpy as np
 
 from .aggregators import LogLikelihood, MdlScore, MutualInformation, NullSink
 from .database import Assignment, Database, InvalidQueryError, QuerySpec
-from .engine import FamilyScorer, GpuContext, GpuDatabase, QueryPlan
+from .engine import FamilyScorer, GpuContext, GpuDatabase, QueryPlan, encode_queries
 from . import _native as N
 
 __all__ = [
@@ -236,10 +236,24 @@ class GpuStrategy(Strategy):
     # -- batched API ------------------------------------------------------------------------
     def query_batch(self, queries, loglik: bool = True, mi: bool = False, nnz: bool = False,
                     tables: bool = False) -> dict:
-        """Run many QuerySpecs in one launch; returns numpy arrays keyed by output name."""
+        """Run many QuerySpecs in one launch; returns numpy arrays keyed by output name.
+
+        Without ``tables`` the batch goes through the one-shot ``cs_query_batch`` (transient
+        plan buffers; big batches plan chunk j+1 while chunk j runs) and ``cells`` /
+        ``table_off`` are None; with ``tables`` a QueryPlan also reports each table's layout.
+        """
         qs = list(queries)
         for q in qs:
             q.validate(self.db)
+        if not tables:
+            ll = np.zeros(len(qs)) if loglik else None
+            mv = np.zeros(len(qs)) if mi else None
+            nz = np.zeros(len(qs), dtype=np.int64) if nnz else None
+            if qs:
+                off, flat = encode_queries([_vars(q) for q in qs])
+                with self._lock:
+                    self.gdb.query_batch(off, flat, 0, loglik=ll, mi=mv, nnz=nz)
+            return {"loglik": ll, "mi": mv, "nnz": nz, "tables": None, "cells": None, "table_off": None}
         with self._lock:
             plan = QueryPlan(self.gdb, [_vars(q) for q in qs], N.CS_WANT_TABLES if tables else 0)
             out = {}

@@ -97,6 +97,9 @@ def test_random_sweep(random_sweep):
         s = cs.GpuStrategy(db)
         qs = [cs.QuerySpec(q["target"], tuple(q["parents"])) for q in d["queries"]]
         out = s.query_batch(qs, loglik=True, nnz=True, tables=True)
+        one_shot = s.query_batch(qs, loglik=True, mi=True, nnz=True)  # cs_query_batch path
+        assert one_shot["tables"] is None and np.array_equal(one_shot["nnz"], out["nnz"])
+        assert all(rel_close(a, b, 1e-12) for a, b in zip(one_shot["loglik"], out["loglik"]))
         for i, q in enumerate(d["queries"]):
             want = golden_records(q)
             c0, c1 = out["table_off"][i], out["table_off"][i] + out["cells"][i]
