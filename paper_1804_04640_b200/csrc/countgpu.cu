@@ -2111,7 +2111,11 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
   // launch tails than its planning costs (cfg2 e2e, 10K queries: one plan 4.08 ms; 2 chunks at
   // growth 2/3/4: 3.89/3.85/3.81; 3 chunks at growth 2/3/4: 4.13/4.01/3.93; cfg3, 289K
   // queries: 30.7 -> 24.5-24.7 ms for 3-5 chunks at growth 2-3)
+  // Score-only batches of cfg2's size lose (LL-only 10K queries: 4.20 ms one plan, 4.62 ms
+  // chunked; the kernels skip the table stores, so chunk j no longer covers chunk j+1's plan):
+  // they are chunked only from 32K queries (cfg3's 289K LL+MDL batch gains 30.7 -> 25 ms).
   int nchunks = env_int("CS_QB_CHUNKS", 0);
+  if (nchunks <= 0 && !tables && nq < env_int("CS_QB_SCORE_MIN", 32768)) nchunks = 1;
   if (nchunks <= 0) {
     const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 2000), 1);
     const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 4), 1), 8);

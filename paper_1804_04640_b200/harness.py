@@ -26,7 +26,7 @@ import numpy as np
 
 from .aggregators import LogLikelihood, MdlScore, MutualInformation, NullSink
 from .database import Assignment, Database, InvalidQueryError, QuerySpec
-from .engine import FamilyScorer, GpuContext, GpuDatabase, QueryPlan, encode_queries
+from .engine import FamilyScorer, GpuContext, GpuDatabase, QueryPlan
 from . import _native as N
 
 __all__ = [
@@ -134,6 +134,15 @@ def load_csv_device(path, delimiter: str | None = None, arities=None, device: in
 # fused aggregators: by exact type, ours or the reference's (duck-typed protocol)
 _FUSED_NAMES = {"LogLikelihood": "loglik", "MdlScore": "mdl", "NullSink": "nnz", "MutualInformation": "mi"}
 _FUSED_MODULES = {LogLikelihood.__module__, "countstream.aggregators"}
+
+
+def _encode_specs(qs) -> tuple[np.ndarray, np.ndarray]:
+    """encode_queries of query objects without per-query tuples (8x faster on 10K queries)."""
+    off = np.zeros(len(qs) + 1, dtype=np.int32)
+    off[1:] = np.cumsum(np.fromiter((len(q.parents) for q in qs), np.int64, len(qs)) + 1)
+    flat = np.fromiter(itertools.chain.from_iterable((q.target, *q.parents) for q in qs), np.int32,
+                       int(off[-1]))
+    return off, flat
 
 
 def _vars(q) -> tuple:
@@ -250,12 +259,12 @@ class GpuStrategy(Strategy):
             mv = np.zeros(len(qs)) if mi else None
             nz = np.zeros(len(qs), dtype=np.int64) if nnz else None
             if qs:
-                off, flat = encode_queries([_vars(q) for q in qs])
+                off, flat = _encode_specs(qs)
                 with self._lock:
                     self.gdb.query_batch(off, flat, 0, loglik=ll, mi=mv, nnz=nz)
             return {"loglik": ll, "mi": mv, "nnz": nz, "tables": None, "cells": None, "table_off": None}
         with self._lock:
-            plan = QueryPlan(self.gdb, [_vars(q) for q in qs], N.CS_WANT_TABLES if tables else 0)
+            plan = QueryPlan(self.gdb, _encode_specs(qs), N.CS_WANT_TABLES if tables else 0)
             out = {}
             ll = np.zeros(len(qs)) if loglik else None
             mv = np.zeros(len(qs)) if mi else None
