@@ -18,8 +18,14 @@
  *     past the call except through a returned handle.
  *   - Query descriptor arrays (var_off, vars, states) are HOST arrays.
  *   - Output arrays may be HOST or DEVICE pointers (detected per pointer).
- *     When every output is a device pointer the call is asynchronous on the
- *     context stream; otherwise it synchronises before returning.
+ *     When every output is a device pointer a single-plan call is asynchronous on
+ *     the context stream; otherwise it synchronises before returning.  A chunked
+ *     cs_query_batch (see there) always synchronises.
+ *   - Thread safety: every call that uses a context (directly or through a
+ *     database / plan handle) holds that context's mutex for its duration, so
+ *     handles may be shared across threads; calls on one context serialise.
+ *   - Row counts: m (and a sharded database's total) must be < 2^32, the range
+ *     of the uint32 count tables (CS_ERR_UNSUPPORTED otherwise).
  *   - No torch, no C++ types cross this boundary.
  *
  * Joint-index convention (reference baselines.py:51-57, survey a11): for a
@@ -173,7 +179,9 @@ int cs_plan_destroy(cs_plan* plan);
 /* create + execute + destroy.  Batches of >= ~4K queries are split into 2-4 chunks (chunk j a
  * 4^j share, first chunk >= 2K queries; env CS_QB_CHUNKS / CS_QB_GROWTH / CS_QB_MIN_CHUNK
  * override) whose host planning overlaps the previous chunk's kernels; outputs land at the same
- * offsets as one plan's (tables in query order, one entry per query in loglik / mi / nnz). */
+ * offsets as one plan's (tables in query order, one entry per query in loglik / mi / nnz).
+ * The whole batch is validated before the first chunk launches (errors name the query's index
+ * in the batch; no output is written), and a chunked call returns synchronised. */
 int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                    uint32_t flags, uint32_t* tables, double* loglik, double* mi, int64_t* nnz);
 

@@ -14,6 +14,10 @@ Two restatements of the reference counting path (reference = countstream,
 * C, algorithmic -- :func:`radix_tables` drives ``radix_oracle.c``, the
   level-wise radix partition of ``radix_query`` (radix.py:33-156), multi-threaded
   over queries; it is the CPU baseline and the oracle at sizes where masks are slow.
+* C, direct -- :func:`dense_tables` (``count_oracle.c``): the joint-key convention of
+  ``_config_keys`` (baselines.py:51-57) counted into a dense table, then LL / MI / nnz;
+  :func:`itemset_supports_enum`: all 2-/3-itemset supports counted record by record.  Used
+  by the full-size parity tests, where the radix port would take minutes.
 
 Pinned by tests/test_oracle_golden.py against golden vectors generated from the
 reference itself (tests/golden/make_golden.py) and the reference's hand-derived KATs.
@@ -55,6 +59,12 @@ def _load():
                                             P, P, P, ctypes.c_int32]
         lib.oracle_bitmap_pack.restype = None
         lib.oracle_bitmap_pack.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P]
+        lib.oracle_dense_tables.restype = ctypes.c_int
+        lib.oracle_dense_tables.argtypes = [P, ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int32, P, P, P,
+                                            P, P, P, P, ctypes.c_int32]
+        lib.oracle_itemset_enum.restype = ctypes.c_int
+        lib.oracle_itemset_enum.argtypes = [P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, P, P,
+                                            ctypes.c_int32]
         lib.oracle_bitmap_counts.restype = ctypes.c_int
         lib.oracle_bitmap_counts.argtypes = [P, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P,
                                              ctypes.c_int32]
@@ -231,3 +241,60 @@ def bitmap_counts(planes: dict, itemsets, m: int, nthreads: int | None = None) -
     lib.oracle_bitmap_counts(ctypes.cast(arr, ctypes.c_void_p), _p(offa), len(itemsets),
                              int(nwords or 0), int(m), _p(out), nthreads or os.cpu_count() or 1)
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# C direct-count restatements (count_oracle.c)
+
+
+def _encode(queries):
+    qs = [tuple(int(v) for v in q) for q in queries]
+    off = np.zeros(len(qs) + 1, dtype=np.int32)
+    if qs:
+        off[1:] = np.cumsum([len(q) for q in qs])
+    flat = np.array([v for q in qs for v in q], dtype=np.int32)
+    return qs, off, flat
+
+
+def dense_tables(cols_u8: np.ndarray, arities, queries, nthreads: int | None = None,
+                 want_tables: bool = True, m: int | None = None):
+    """Direct dense count of ``queries`` (variable tuples, target first) over the first ``m``
+    rows of ``cols_u8`` (n x ld, default all).
+
+    Returns (tables uint32 packed | None, table_off int64, loglik, mi, nnz).
+    """
+    lib = _load()
+    cols = np.ascontiguousarray(cols_u8, dtype=np.uint8)
+    n, ld = cols.shape
+    m = ld if m is None else int(m)
+    ar = np.ascontiguousarray(arities, dtype=np.int32)
+    qs, off, flat = _encode(queries)
+    cells = np.array([int(np.prod([int(ar[v]) for v in q], dtype=np.int64)) for q in qs], dtype=np.int64)
+    toff = np.zeros(len(qs), dtype=np.int64)
+    if len(qs):
+        toff[1:] = np.cumsum(cells)[:-1]
+    tables = np.zeros(int(cells.sum()), dtype=np.uint32) if want_tables else None
+    ll = np.zeros(len(qs))
+    mi = np.zeros(len(qs))
+    nnz = np.zeros(len(qs), dtype=np.int64)
+    if qs:
+        rc = lib.oracle_dense_tables(_p(cols), ld, m, _p(ar), len(qs), _p(off), _p(flat), _p(toff),
+                                     _p(tables), _p(ll), _p(mi), _p(nnz), nthreads or os.cpu_count() or 1)
+        if rc != 0:
+            raise RuntimeError(f"oracle_dense_tables failed: {rc}")
+    return tables, toff, ll, mi, nnz
+
+
+def itemset_supports_enum(item_cols: np.ndarray, nthreads: int | None = None, m: int | None = None):
+    """(pairs (n, n) int64 with [a, b] for a < b, triples int64 in itertools.combinations order)
+    of the n binary item columns (rows = items, state 1 = present)."""
+    lib = _load()
+    cols = np.ascontiguousarray(item_cols, dtype=np.uint8)
+    n, ld = cols.shape
+    m = ld if m is None else int(m)
+    pairs = np.zeros((n, n), dtype=np.int64)
+    triples = np.zeros(max(n * (n - 1) * (n - 2) // 6, 1), dtype=np.int64)
+    rc = lib.oracle_itemset_enum(_p(cols), ld, m, n, _p(pairs), _p(triples), nthreads or os.cpu_count() or 1)
+    if rc != 0:
+        raise RuntimeError(f"oracle_itemset_enum failed: {rc}")
+    return pairs, triples[: n * (n - 1) * (n - 2) // 6]

@@ -81,24 +81,49 @@ class EngineError(RuntimeError):
         self.code = code
 
 
-def _load() -> ctypes.CDLL:
+def _require() -> None:
     if not LIB_PATH.exists():
         raise ImportError(
             f"libcountgpu.so not found at {LIB_PATH}; build it with "
             "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)"
         )
+
+
+def _load() -> ctypes.CDLL:
+    _require()
     lib = ctypes.CDLL(str(LIB_PATH))
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.cs_abi_version() != 1:  # pragma: no cover - build skew
+        raise ImportError(f"libcountgpu ABI {lib.cs_abi_version()} != 1")
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """The library handle, mapped into the process on the first call into it (not at import):
+    importing the package for its host-side pieces (workload builders, query objects -- e.g.
+    bench.py's reference arm) does not load the engine.  A missing library still fails at
+    import (the check below), and every call goes to the CUDA engine: there is no fallback."""
 
-if lib.cs_abi_version() != 1:  # pragma: no cover - build skew
-    raise ImportError(f"libcountgpu ABI {lib.cs_abi_version()} != 1")
+    _lib: ctypes.CDLL | None = None
+
+    def _get(self) -> ctypes.CDLL:
+        if _LazyLib._lib is None:
+            _LazyLib._lib = _load()
+        return _LazyLib._lib
+
+    @property
+    def loaded(self) -> bool:
+        return _LazyLib._lib is not None
+
+    def __getattr__(self, name):
+        return getattr(self._get(), name)
+
+
+_require()
+lib = _LazyLib()
 
 
 def check(rc: int) -> None:

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <ctime>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -117,6 +118,10 @@ static int hist_path(const QDesc& d) {
 // handles
 
 struct cs_ctx {
+  // every entry point that touches the context's stream, scratch, staging, pipelining bank or
+  // events holds this (recursive: cs_query_batch re-enters cs_plan_execute); a context shared by
+  // several databases / strategies / threads therefore serialises their calls
+  std::recursive_mutex mu;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -263,6 +268,18 @@ struct cs_plan {
   } sl[2];
 };
 
+struct CtxLock {  // RAII hold of cs_ctx::mu (NULL handles are reported by the callee)
+  cs_ctx* c;
+  explicit CtxLock(cs_ctx* x) : c(x) {
+    if (c) c->mu.lock();
+  }
+  ~CtxLock() {
+    if (c) c->mu.unlock();
+  }
+  CtxLock(const CtxLock&) = delete;
+  CtxLock& operator=(const CtxLock&) = delete;
+};
+
 // ------------------------------------------------------------------------------------------
 // library / context
 
@@ -359,6 +376,7 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
 }
 
 extern "C" int cs_ctx_set_stream(cs_ctx* ctx, void* stream) {
+  CtxLock lk_(ctx);
   if (!ctx) return fail(CS_ERR_INVALID, "cs_ctx_set_stream: NULL ctx");
   if (ctx->own_stream && ctx->stream) {
     cudaStreamSynchronize(ctx->stream);
@@ -387,6 +405,7 @@ extern "C" int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches) {
 }
 
 extern "C" int cs_ctx_last_kernel_ms(cs_ctx* ctx, float* ms) {
+  CtxLock lk_(ctx);
   if (!ctx || !ms) return fail(CS_ERR_INVALID, "cs_ctx_last_kernel_ms: NULL argument");
   *ms = 0.f;
   if (!ctx->ev_valid) return CS_OK;
@@ -466,6 +485,9 @@ static int db_alloc(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities, c
     return fail(CS_ERR_INVALID, "database must have at least one variable and one row, got n=%d m=%lld",
                 n, (long long)m);
   if (!arities) return fail(CS_ERR_INVALID, "cs_db: arities is NULL");
+  if (m > (int64_t)UINT32_MAX)
+    return fail(CS_ERR_UNSUPPORTED, "database has %lld rows; the uint32 count tables hold at most 2^32-1 records",
+                (long long)m);
   for (int i = 0; i < n; ++i) {
     if (arities[i] < 1) return fail(CS_ERR_INVALID, "every arity must be at least 1 (variable %d)", i);
     if (arities[i] > CS_MAX_ARITY)
@@ -521,11 +543,13 @@ static int db_pack(cs_db* db, int32_t var0, int32_t nvars) {
 
 extern "C" int cs_db_create_empty(cs_ctx* ctx, int32_t n, int64_t m, const int32_t* arities,
                                   cs_db** out) {
+  CtxLock lk_(ctx);
   return db_alloc(ctx, n, m, arities, out);
 }
 
 extern "C" int cs_db_create(cs_ctx* ctx, const uint8_t* cols, int32_t n, int64_t m, int64_t ld,
                             const int32_t* arities, cs_db** out) {
+  CtxLock lk_(ctx);
   if (!cols) return fail(CS_ERR_INVALID, "cs_db_create: cols is NULL");
   if (ld < m) return fail(CS_ERR_INVALID, "cs_db_create: ld %lld < m %lld", (long long)ld, (long long)m);
   cs_db* db = nullptr;
@@ -536,8 +560,8 @@ extern "C" int cs_db_create(cs_ctx* ctx, const uint8_t* cols, int32_t n, int64_t
   unsigned long long* d_bad = nullptr;
   CS_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long) * n));
   CS_CUDA(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long) * n, ctx->stream));
-  dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 1024), n);
-  k_check_states<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, m, db->d_arity, d_bad);
+  dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 1024), (unsigned)std::min(n, 65535));
+  k_check_states<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, m, db->d_arity, d_bad, n);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
   std::vector<unsigned long long> bad(n);
@@ -565,6 +589,7 @@ extern "C" int cs_db_create(cs_ctx* ctx, const uint8_t* cols, int32_t n, int64_t
 extern "C" int cs_db_generate(cs_db* db, int32_t var, uint64_t seed, int64_t row_offset,
                               int32_t nparents, const int32_t* parents, const uint32_t* thresholds,
                               int64_t nthresholds) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db) return fail(CS_ERR_INVALID, "cs_db_generate: NULL db");
   if (var < 0 || var >= db->n) return fail(CS_ERR_INVALID, "cs_db_generate: bad var %d", var);
   if (nparents < 0 || nparents > CS_MAXK) return fail(CS_ERR_INVALID, "cs_db_generate: nparents %d", nparents);
@@ -614,6 +639,7 @@ extern "C" int cs_db_generate(cs_db* db, int32_t var, uint64_t seed, int64_t row
 }
 
 extern "C" int cs_db_destroy(cs_db* db) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db) return CS_OK;
   cudaSetDevice(db->ctx->device);
   cudaStreamSynchronize(db->ctx->stream);
@@ -643,6 +669,7 @@ extern "C" int cs_db_columns(cs_db* db, const uint8_t** dev, int64_t* ld) {
 }
 
 extern "C" int cs_db_download(cs_db* db, int32_t var, int64_t row0, int64_t nrows, uint8_t* host) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db || !host) return fail(CS_ERR_INVALID, "cs_db_download: NULL argument");
   if (var < 0 || var >= db->n || row0 < 0 || nrows < 0 || row0 + nrows > db->m)
     return fail(CS_ERR_INVALID, "cs_db_download: out of range");
@@ -661,6 +688,9 @@ extern "C" int cs_db_arities(cs_db* db, int32_t* arities) {
 
 extern "C" int cs_db_set_total_rows(cs_db* db, int64_t m_total) {
   if (!db || m_total < db->m) return fail(CS_ERR_INVALID, "cs_db_set_total_rows: bad argument");
+  if (m_total > (int64_t)UINT32_MAX)
+    return fail(CS_ERR_UNSUPPORTED, "%lld total rows: merged uint32 count tables hold at most 2^32-1 records",
+                (long long)m_total);
   db->m_total = m_total;
   return CS_OK;
 }
@@ -778,6 +808,7 @@ int h2d_large(cs_ctx* ctx, void* dst, const void* src, size_t bytes) {
 
 extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, int32_t delim,
                                const int32_t* arities, int32_t n_arities, cs_db** out, int64_t* info) {
+  CtxLock lk_(ctx);
   if (!ctx || !out || !info || (!text && nbytes > 0) || nbytes < 0)
     return fail(CS_ERR_INVALID, "cs_db_load_text: bad argument");
   if (delim < CS_DELIM_WHITESPACE || delim > 255)
@@ -917,8 +948,8 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
   }
   const bool shift = hmin == 1;
   if (shift) {
-    dim3 g((unsigned)std::min<int64_t>((nrec / 4 + 255) / 256 + 1, 1024), (unsigned)width);
-    k_txt_shift<<<g, 256, 0, st>>>(db->cols, db->ld, nrec);
+    dim3 g((unsigned)std::min<int64_t>((nrec / 4 + 255) / 256 + 1, 1024), (unsigned)std::min<int64_t>(width, 65535));
+    k_txt_shift<<<g, 256, 0, st>>>(db->cols, db->ld, nrec, (int)width);
     ctx->launches++;
     if (cudaGetLastError() != cudaSuccess) return drop(fail(CS_ERR_CUDA, "k_txt_shift launch failed"));
   }
@@ -946,7 +977,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
         cudaMemcpyAsync(db->d_arity + i, &ai, sizeof(int32_t), cudaMemcpyHostToDevice, st);
         cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st);
         dim3 g((unsigned)std::min<int64_t>((nrec + 255) / 256, 1024), 1);
-        k_check_states<<<g, 256, 0, st>>>(db->cols + i * db->ld, db->ld, nrec, db->d_arity + i, dbad);
+        k_check_states<<<g, 256, 0, st>>>(db->cols + i * db->ld, db->ld, nrec, db->d_arity + i, dbad, 1);
         ctx->launches++;
         unsigned long long row = 0;
         uint8_t state = 0;
@@ -983,6 +1014,7 @@ extern "C" int cs_db_load_text(cs_ctx* ctx, const char* text, int64_t nbytes, in
 // bitmap index
 
 extern "C" int cs_bitmap_build(cs_db* db, int32_t nvars, const int32_t* vars) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db) return fail(CS_ERR_INVALID, "cs_bitmap_build: NULL db");
   std::vector<int32_t> list;
   if (!vars || nvars < 0) {
@@ -1024,9 +1056,9 @@ extern "C" int cs_bitmap_build(cs_db* db, int32_t nvars, const int32_t* vars) {
   CS_CUDA(cudaMalloc(&d_off, sizeof(int64_t) * list.size()));
   CS_CUDA(cudaMemcpyAsync(d_vars, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice, ctx->stream));
   CS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * list.size(), cudaMemcpyHostToDevice, ctx->stream));
-  dim3 grid((unsigned)std::min<int64_t>((words + 255) / 256, 4096), (unsigned)list.size());
+  dim3 grid((unsigned)std::min<int64_t>((words + 255) / 256, 4096), (unsigned)std::min<size_t>(list.size(), 65535));
   k_bitmap_build<<<grid, 256, 0, ctx->stream>>>(db->cols, db->ld, db->m, d_vars, db->d_arity, d_off,
-                                                 db->planes, words);
+                                                 db->planes, words, (int)list.size());
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
   // per-plane record counts (the index's state counts): the itemset planner ranks items by them
@@ -1034,7 +1066,8 @@ extern "C" int cs_bitmap_build(cs_db* db, int32_t nvars, const int32_t* vars) {
   unsigned long long* d_cnt = nullptr;
   CS_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long) * nplanes));
   CS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * nplanes, ctx->stream));
-  k_plane_popc<<<dim3(8, (unsigned)nplanes), 256, 0, ctx->stream>>>(db->planes, words, d_cnt);
+  k_plane_popc<<<dim3(8, (unsigned)std::min<int64_t>(nplanes, 65535)), 256, 0, ctx->stream>>>(db->planes, words,
+                                                                                               d_cnt, nplanes);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
   db->plane_count.assign(nplanes, 0);
@@ -1061,7 +1094,7 @@ extern "C" int cs_bitmap_plane(cs_db* db, int32_t var, int32_t state, const uint
 // planning
 
 static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
-                      uint32_t flags, cs_plan** out, bool transient = false) {
+                      uint32_t flags, cs_plan** out, bool transient = false, int32_t qbase = 0) {
   if (!db || !out) return fail(CS_ERR_INVALID, "cs_plan_create: NULL argument");
   if (nq < 0) return fail(CS_ERR_INVALID, "cs_plan_create: nq < 0");
   if (nq > 0 && (!var_off || !vars)) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
@@ -1094,7 +1127,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     const int b = var_off[q], e = var_off[q + 1];
     const int k = e - b;
     if (k < 1) {
-      return fail(CS_ERR_INVALID, "query %d has no target variable", q);
+      return fail(CS_ERR_INVALID, "query %d has no target variable", qbase + q);
     }
     QDesc d;
     memset(&d, 0, sizeof d);
@@ -1107,14 +1140,14 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
       for (int j = 0; j < i; ++j)
         if (vars[b + j] == v) {
-          return fail(CS_ERR_INVALID, "query %d repeats variable %d", q, v);
+          return fail(CS_ERR_INVALID, "query %d repeats variable %d", qbase + q, v);
         }
       if (i < CS_MAXK) {
         d.coff[i] = (uint32_t)((int64_t)v * (db->ld / 256));
         d.stride[i] = (uint32_t)c;
       }
       if (c > (int64_t)(((uint64_t)1 << 63) - 1) / db->arity[v]) {
-        return fail(CS_ERR_UNSUPPORTED, "query %d: joint state space exceeds 2^63 cells", q);
+        return fail(CS_ERR_UNSUPPORTED, "query %d: joint state space exceeds 2^63 cells", qbase + q);
       }
       c *= db->arity[v];
       if (c <= 256) nbyte = i + 1;
@@ -1122,7 +1155,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     d.base = db->cols;
     const bool sparse = c > ((int64_t)1 << max_dense);
     if (sparse && (flags & F_PARTIAL)) {
-      return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", q);
+      return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", qbase + q);
     }
     d.k = k;
     d.cells = sparse ? 0u : (uint32_t)c;
@@ -1152,11 +1185,19 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.mode = (c << rl) <= 16384 ? 0 : (c <= 65536 ? 1 : 2);
       // 16-bit counters (two cells per word) double the replicas when 32-bit ones are short of
       // 32; counters cannot overflow while every replica serves <= 65535 rows of an item
-      const int64_t seg_cap = std::min<int64_t>(m, knob_seg_max);
+      const int64_t seg_cap = std::min<int64_t>(round_up(m, 256), knob_seg_max);
       if (d.rlog < 5 && c <= 65536 && knob_half) {
         int rh = 0;
         while (rh < 5 && (((c + 1) / 2) << (rh + 1)) <= smem_words) ++rh;
-        if (rh > d.rlog && seg_cap <= (65535LL << rh)) {
+        // the busiest replica: thread t takes vectors t, t + 1024, ... (RPV rows each, padding
+        // included), so a replica of 1024 / R threads counts up to ceil(nvec / 1024) * (1024 / R)
+        // * RPV rows -- for every column layout the query may read
+        int64_t busiest = 0;
+        for (int64_t rpv = 16; rpv <= 64; rpv *= 2) {
+          const int64_t nvec = (seg_cap + rpv - 1) / rpv;
+          busiest = std::max(busiest, (nvec + CS_HIST_THREADS - 1) / CS_HIST_THREADS * (CS_HIST_THREADS >> rh) * rpv);
+        }
+        if (rh > d.rlog && busiest <= 65535) {
           d.half = 1;
           d.rlog = rh;
         }
@@ -1601,6 +1642,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
 
 extern "C" int cs_plan_create(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                               uint32_t flags, cs_plan** out) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   int rc = plan_build(db, nq, var_off, vars, flags, out);
   if (rc == CS_OK) {
     // the staging copy must land before the caller may reuse the pinned buffer
@@ -1618,6 +1660,7 @@ extern "C" int cs_plan_info(cs_plan* p, int64_t* cells, int64_t* table_off, int6
 }
 
 extern "C" int cs_plan_destroy(cs_plan* p) {
+  CtxLock lk_(p ? p->db->ctx : nullptr);
   if (!p) return CS_OK;
   cudaSetDevice(p->db->ctx->device);
   for (auto& sq : p->sparse)
@@ -1866,6 +1909,7 @@ static int run_chunked_score(cs_plan* p, int which, const uint32_t* dtab, uint32
 
 extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, double* mi,
                                int64_t* nnz) {
+  CtxLock lk_(p ? p->db->ctx : nullptr);
   if (!p) return fail(CS_ERR_INVALID, "cs_plan_execute: NULL plan");
   cs_db* db = p->db;
   cs_ctx* ctx = db->ctx;
@@ -1913,9 +1957,10 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     }
   }
   if (!p->generic_list.empty()) {
-    dim3 grid((unsigned)std::min<int64_t>((db->m + 255) / 256, 1024), (unsigned)p->generic_list.size());
+    dim3 grid((unsigned)std::min<int64_t>((db->m + 255) / 256, 1024),
+              (unsigned)std::min<size_t>(p->generic_list.size(), 65535));
     k_hist_generic<<<grid, 256, 0, ctx->stream>>>(p->d_q, p->d_generic_list, p->d_gvars, p->d_gstride,
-                                                  db->cols, db->ld, db->m, dtab);
+                                                  db->cols, db->ld, db->m, dtab, (int)p->generic_list.size());
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
   }
@@ -1955,6 +2000,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
 
 extern "C" int cs_plan_score(cs_plan* p, const uint32_t* tables, double* loglik, double* mi,
                              int64_t* nnz) {
+  CtxLock lk_(p ? p->db->ctx : nullptr);
   if (!p) return fail(CS_ERR_INVALID, "cs_plan_score: NULL plan");
   cs_ctx* ctx = p->db->ctx;
   CS_CUDA(cudaSetDevice(ctx->device));
@@ -1977,6 +2023,7 @@ extern "C" int cs_plan_score(cs_plan* p, const uint32_t* tables, double* loglik,
 
 extern "C" int cs_plan_compact(cs_plan* p, const uint32_t* tables, const int64_t* out_off,
                                int64_t total_nnz, int64_t* cell_idx, int64_t* n_ijk, int64_t* n_ij) {
+  CtxLock lk_(p ? p->db->ctx : nullptr);
   if (!p || !out_off || !cell_idx || !n_ijk || !n_ij)
     return fail(CS_ERR_INVALID, "cs_plan_compact: NULL argument");
   cs_ctx* ctx = p->db->ctx;
@@ -2019,6 +2066,7 @@ extern "C" int cs_plan_compact(cs_plan* p, const uint32_t* tables, const int64_t
 extern "C" int cs_family_scores(cs_ctx* ctx, int64_t nfam, const double* nlogn, int64_t nsub,
                                 const int32_t* s_idx, const int32_t* p_idx, const double* penalty,
                                 double m_ln_m, double* ll, double* mdl) {
+  CtxLock lk_(ctx);
   if (!ctx || nfam < 0 || nsub < 0) return fail(CS_ERR_INVALID, "cs_family_scores: bad argument");
   if (nfam == 0) return CS_OK;
   if (!nlogn || !s_idx || !p_idx || (mdl && !penalty))
@@ -2073,6 +2121,28 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
       cudaStreamSynchronize(c->stream);
     }
   } restore{ctx};
+  {
+    // validate the whole batch before the first chunk launches, so a bad query leaves every
+    // output untouched (the per-chunk plans would otherwise fail after earlier chunks wrote)
+    const int64_t max_dense = (int64_t)env_int("CS_MAX_DENSE_LOG2", 30);
+    for (int32_t q = 0; q < nq; ++q) {
+      const int b = var_off[q], e = var_off[q + 1];
+      if (e - b < 1) return fail(CS_ERR_INVALID, "query %d has no target variable", q);
+      uint64_t c = 1;
+      for (int i = b; i < e; ++i) {
+        const int v = vars[i];
+        if (v < 0 || v >= db->n)
+          return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
+        for (int j = b; j < i; ++j)
+          if (vars[j] == v) return fail(CS_ERR_INVALID, "query %d repeats variable %d", q, v);
+        if (c > (((uint64_t)1 << 63) - 1) / (uint64_t)db->arity[v])
+          return fail(CS_ERR_UNSUPPORTED, "query %d: joint state space exceeds 2^63 cells", q);
+        c *= (uint64_t)db->arity[v];
+      }
+      if ((flags & F_PARTIAL) && c > ((uint64_t)1 << max_dense))
+        return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", q);
+    }
+  }
   ctx->pipe = true;
   int64_t cell_off = 0, wcum = 0;
   int32_t q0 = 0;
@@ -2084,7 +2154,7 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
     ctx->bank = j & 1;
     cs_plan* p = nullptr;
     const double t0 = trace ? now_ms() : 0.0;
-    CS_TRY(plan_build(db, q1 - q0, var_off + q0, vars, flags, &p, /*transient=*/true));
+    CS_TRY(plan_build(db, q1 - q0, var_off + q0, vars, flags, &p, /*transient=*/true, q0));
     if (trace) tplan += now_ms() - t0;
     const int rc = cs_plan_execute(p, tables ? tables + cell_off : nullptr, loglik ? loglik + q0 : nullptr,
                                    mi ? mi + q0 : nullptr, nnz ? nnz + q0 : nullptr);
@@ -2103,6 +2173,7 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
 extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                               uint32_t flags, uint32_t* tables, double* loglik, double* mi,
                               int64_t* nnz) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   cs_plan* p = nullptr;
   const bool trace = env_int("CS_TRACE", 0) != 0;
   // big batches: plan chunk j+1 on the host while chunk j's kernels run (chunk sizes double,
@@ -2145,6 +2216,7 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
 
 extern "C" int cs_count_points(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                                const int32_t* states, int64_t* counts) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db || !counts) return fail(CS_ERR_INVALID, "cs_count_points: NULL argument");
   if (nq < 0) return fail(CS_ERR_INVALID, "cs_count_points: nq < 0");
   if (nq == 0) return CS_OK;
@@ -2197,15 +2269,15 @@ extern "C" int cs_count_points(cs_db* db, int32_t nq, const int32_t* var_off, co
     unsigned long long* dc = (unsigned long long*)(d + o4);
     if (all_planes) {
       const int64_t wpc = 32768;
-      dim3 grid((unsigned)((db->words + wpc - 1) / wpc), (unsigned)nne);
+      dim3 grid((unsigned)((db->words + wpc - 1) / wpc), (unsigned)std::min(nne, 65535));
       k_points_bitmap<<<grid, 256, 0, ctx->stream>>>((const int32_t*)d, (const int64_t*)(d + o1),
-                                                      db->planes, db->words, wpc, dc);
+                                                      db->planes, db->words, wpc, dc, nne);
     } else {
       const int64_t rpc = 1 << 20;
-      dim3 grid((unsigned)((db->m + rpc - 1) / rpc), (unsigned)nne);
+      dim3 grid((unsigned)((db->m + rpc - 1) / rpc), (unsigned)std::min(nne, 65535));
       k_points_scan<<<grid, 256, 0, ctx->stream>>>((const int32_t*)d, (const int32_t*)(d + o2),
                                                     (const int32_t*)(d + o3), db->cols, db->ld, db->m,
-                                                    rpc, dc);
+                                                    rpc, dc, nne);
     }
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
@@ -2347,6 +2419,7 @@ static int itemsets_selector(cs_db* db, int n, const std::vector<const uint32_t*
 
 extern "C" int cs_itemset_supports(cs_db* db, int32_t nitems, const int32_t* items, int64_t* pairs,
                                    int64_t* triples) {
+  CtxLock lk_(db ? db->ctx : nullptr);
   if (!db) return fail(CS_ERR_INVALID, "cs_itemset_supports: NULL db");
   if (nitems < 0 || nitems > 30000) return fail(CS_ERR_INVALID, "cs_itemset_supports: nitems %d", nitems);
   if (nitems == 0 || (!pairs && !triples)) return CS_OK;

@@ -429,13 +429,15 @@ __global__ void __launch_bounds__(TX_THREADS) k_txt_parse_thr(
 }
 
 // 1-based file: every state of rows [0, m) minus one (mod 256: a 256 stored as 0 becomes 255).
-__global__ void k_txt_shift(uint8_t* __restrict__ cols, int64_t ld, int64_t m) {
-  uint32_t* c = reinterpret_cast<uint32_t*>(cols + (int64_t)blockIdx.y * ld);
-  const int64_t nw = (m + 3) >> 2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t left = m - 4 * i;
-    const uint32_t sub = left >= 4 ? 0x01010101u : (0x01010101u & ((1u << (8 * left)) - 1));
-    c[i] = __vsub4(c[i], sub);
+__global__ void k_txt_shift(uint8_t* __restrict__ cols, int64_t ld, int64_t m, int n) {
+  for (int var = blockIdx.y; var < n; var += gridDim.y) {
+    uint32_t* c = reinterpret_cast<uint32_t*>(cols + (int64_t)var * ld);
+    const int64_t nw = (m + 3) >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t left = m - 4 * i;
+      const uint32_t sub = left >= 4 ? 0x01010101u : (0x01010101u & ((1u << (8 * left)) - 1));
+      c[i] = __vsub4(c[i], sub);
+    }
   }
 }
 

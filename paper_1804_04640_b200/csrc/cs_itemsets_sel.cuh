@@ -38,17 +38,20 @@ struct SelUnit {
 
 // record count of each of the bitmap index's planes (contiguous, `words` uint32 each): the
 // index's state counts, taken once when it is built
-__global__ void k_plane_popc(const uint32_t* __restrict__ planes, int64_t words, unsigned long long* __restrict__ cnt) {
-  const uint4* p = reinterpret_cast<const uint4*>(planes + (int64_t)blockIdx.y * words);
-  const int64_t nv = words >> 2;
-  uint32_t c = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 x = __ldg(p + i);
-    c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-  }
+__global__ void k_plane_popc(const uint32_t* __restrict__ planes, int64_t words, unsigned long long* __restrict__ cnt,
+                             int64_t nplanes) {
+  for (int64_t pl = blockIdx.y; pl < nplanes; pl += gridDim.y) {
+    const uint4* p = reinterpret_cast<const uint4*>(planes + pl * words);
+    const int64_t nv = words >> 2;
+    uint32_t c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+      const uint4 x = __ldg(p + i);
+      c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + blockIdx.y, (unsigned long long)c);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + pl, (unsigned long long)c);
+  }
 }
 
 // rank_plane[k] = state-1 plane of the item of rank k (k < n); wr = words per record mask (1..8).

@@ -860,16 +860,18 @@ __global__ void __launch_bounds__(512, 2)
 __global__ void k_hist_generic(const QDesc* __restrict__ qd, const int32_t* __restrict__ qlist,
                                const int32_t* __restrict__ gvars,
                                const uint32_t* __restrict__ gstride, const uint8_t* __restrict__ cols,
-                               int64_t ld, int64_t m, uint32_t* tables) {
-  const QDesc q = qd[qlist[blockIdx.y]];
-  uint32_t* t = tables + q.table_off;
-  const int32_t* vv = gvars + q.var_base;
-  const uint32_t* ss = gstride + q.var_base;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t idx = 0;
-    for (int v = 0; v < q.k; ++v) idx += (uint32_t)__ldg(cols + (int64_t)vv[v] * ld + row) * ss[v];
-    atomicAdd(t + idx, 1u);
+                               int64_t ld, int64_t m, uint32_t* tables, int nlist) {
+  for (int li = blockIdx.y; li < nlist; li += gridDim.y) {  // grid.y <= 65535: stride over queries
+    const QDesc q = qd[qlist[li]];
+    uint32_t* t = tables + q.table_off;
+    const int32_t* vv = gvars + q.var_base;
+    const uint32_t* ss = gstride + q.var_base;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
+         row += (int64_t)gridDim.x * blockDim.x) {
+      uint32_t idx = 0;
+      for (int v = 0; v < q.k; ++v) idx += (uint32_t)__ldg(cols + (int64_t)vv[v] * ld + row) * ss[v];
+      atomicAdd(t + idx, 1u);
+    }
   }
 }
 
@@ -1227,13 +1229,14 @@ __global__ void k_pack2(const uint8_t* __restrict__ cols, int64_t ld, uint8_t* _
 
 // state validation: bad[var] = first row whose state >= arity (or INT64_MAX)
 __global__ void k_check_states(const uint8_t* __restrict__ cols, int64_t ld, int64_t m,
-                               const int32_t* __restrict__ arity, unsigned long long* bad) {
-  const int var = blockIdx.y;
-  const uint32_t r = (uint32_t)arity[var];
-  const uint8_t* c = cols + (int64_t)var * ld;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    if ((uint32_t)c[row] >= r) atomicMin(bad + var, (unsigned long long)row);
+                               const int32_t* __restrict__ arity, unsigned long long* bad, int n) {
+  for (int var = blockIdx.y; var < n; var += gridDim.y) {
+    const uint32_t r = (uint32_t)arity[var];
+    const uint8_t* c = cols + (int64_t)var * ld;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
+         row += (int64_t)gridDim.x * blockDim.x) {
+      if ((uint32_t)c[row] >= r) atomicMin(bad + var, (unsigned long long)row);
+    }
   }
 }
 
@@ -1247,8 +1250,8 @@ __device__ __forceinline__ uint32_t eq_bits4(uint32_t x, uint32_t pat) {
 __global__ void k_bitmap_build(const uint8_t* __restrict__ cols, int64_t ld, int64_t m,
                                const int32_t* __restrict__ vars, const int32_t* __restrict__ arity,
                                const int64_t* __restrict__ plane_off, uint32_t* planes,
-                               int64_t words) {
-  const int vi = blockIdx.y;
+                               int64_t words, int nvars) {
+  for (int vi = blockIdx.y; vi < nvars; vi += gridDim.y) {
   const int var = vars[vi];
   const int r = arity[var];
   const uint8_t* c = cols + (int64_t)var * ld;
@@ -1274,15 +1277,16 @@ __global__ void k_bitmap_build(const uint8_t* __restrict__ cols, int64_t ld, int
       out[(int64_t)s * words + w] = bits & valid;
     }
   }
+  }
 }
 
 // K4 (bitmap): counts[q] += popc(AND_j plane_j) over a word chunk.  grid = (chunks, nq).
 // plist holds, per query, k plane offsets starting at poff[q].
 __global__ void k_points_bitmap(const int32_t* __restrict__ poff, const int64_t* __restrict__ plist,
                                 const uint32_t* __restrict__ planes, int64_t words,
-                                int64_t words_per_chunk, unsigned long long* counts) {
+                                int64_t words_per_chunk, unsigned long long* counts, int nq) {
   __shared__ unsigned long long s_red[32];
-  const int q = blockIdx.y;
+  for (int q = blockIdx.y; q < nq; q += gridDim.y) {  // grid.y <= 65535: stride over queries
   const int b = poff[q], k = poff[q + 1] - b;
   const int64_t w0 = (int64_t)blockIdx.x * words_per_chunk;
   const int64_t w1 = min(words, w0 + words_per_chunk);
@@ -1297,15 +1301,16 @@ __global__ void k_points_bitmap(const int32_t* __restrict__ poff, const int64_t*
   }
   const unsigned long long t = block_sum_u64(acc, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(counts + q, t);
+  }
 }
 
 // K4 (byte scan): rows where every listed column equals its state.  grid = (chunks, nq).
 __global__ void k_points_scan(const int32_t* __restrict__ poff, const int32_t* __restrict__ pvar,
                               const int32_t* __restrict__ pstate, const uint8_t* __restrict__ cols,
                               int64_t ld, int64_t m, int64_t rows_per_chunk,
-                              unsigned long long* counts) {
+                              unsigned long long* counts, int nq) {
   __shared__ unsigned long long s_red[32];
-  const int q = blockIdx.y;
+  for (int q = blockIdx.y; q < nq; q += gridDim.y) {
   const int b = poff[q], k = poff[q + 1] - b;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_chunk;
   const int64_t r1 = min(m, r0 + rows_per_chunk);
@@ -1334,6 +1339,7 @@ __global__ void k_points_scan(const int32_t* __restrict__ poff, const int32_t* _
   }
   const unsigned long long t = block_sum_u64(acc, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(counts + q, t);
+  }
 }
 
 }  // namespace cs

@@ -58,3 +58,24 @@ def test_package_has_no_cpu_fallback():
         src = p.read_text()
         assert not re.search(r"^\s*(import|from)\s+(oracle|gen_twin)\b", src, re.M), p
         assert "sys.path" not in src, p
+
+
+def test_library_maps_on_first_call_not_at_import():
+    """Importing the package (workload builders, query objects) does not map libcountgpu.so --
+    bench.py's reference arm imports them and must run without the engine in the process --
+    while the first call into the ABI does (and a missing library still fails at import)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1804_04640_b200 as cs\n"
+        "from paper_1804_04640_b200 import workloads, _native\n"
+        "w = workloads.cfg1(nq=5)\n"
+        "maps = lambda: 'libcountgpu' in open('/proc/self/maps').read()\n"
+        "before = maps()\n"
+        "_native.lib.cs_abi_version()\n"
+        "print(before, maps(), _native.lib.loaded)\n" % str(ROOT)
+    )
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout
+    assert out.split() == ["False", "True", "True"]

@@ -127,3 +127,65 @@ def test_mi_definition():
     ll0 = O.loglik_of_records(O.oracle_records(cols, [3, 3], 1, ()))
     assert abs(mi - (ll1 - ll0) / 400) < 1e-12
     assert mi > 0
+
+
+# ---- the direct-count restatements (count_oracle.c) used by the full-size parity tests ------
+
+
+def test_dense_tables_reference_cases(reference_cases):
+    for name, case in reference_cases.items():
+        if "queries" not in case:
+            continue
+        db = case_db(case)
+        queries = [(q["target"], *q["parents"]) for q in case["queries"]]
+        tabs, off, ll, mi, nnz = O.dense_tables(db.columns_u8(), db.arities, queries, nthreads=2)
+        for i, q in enumerate(case["queries"]):
+            want = golden_records(q)
+            cells = int(np.prod([db.arities[v] for v in queries[i]]))
+            got = O.records_from_table(tabs[off[i]:off[i] + cells], q["target"], q["parents"], db.arities)
+            assert got == want, (name, i)
+            assert nnz[i] == len(want)
+            assert rel_close(ll[i], q["loglik"], 1e-12)
+            assert abs(mi[i] - O.mi_of_records(want, db.m)) <= 1e-12 * max(1.0, abs(ll[i]) / db.m)
+
+
+def test_dense_tables_random_sweep_and_cfg1(random_sweep, cfg1_golden):
+    for d in random_sweep["dbs"]:
+        db = sweep_db(d)
+        queries = [(q["target"], *q["parents"]) for q in d["queries"]]
+        tabs, off, ll, mi, nnz = O.dense_tables(db.columns_u8(), db.arities, queries, nthreads=2)
+        rt, _, rll, _ = O.radix_tables(db.columns_u8(), db.arities, queries, nthreads=2)
+        assert np.array_equal(tabs, rt)
+        for i, q in enumerate(d["queries"]):
+            assert rel_close(ll[i], q["loglik"], 1e-12)
+    g = cfg1_golden
+    queries = [tuple(int(v) for v in q) for q in g["queries"]]
+    tabs, off, ll, _, _ = O.dense_tables(g["data"], g["arities"], queries)
+    assert np.array_equal(off, g["table_off"]) and np.array_equal(tabs, g["tables"])
+    assert np.allclose(ll, g["loglik"], rtol=1e-12, atol=0)
+    # without tables (internal scratch), and over a row prefix of a wider array
+    _, _, ll2, _, _ = O.dense_tables(g["data"], g["arities"], queries, want_tables=False)
+    assert np.array_equal(ll, ll2)
+    wide = np.hstack([g["data"], np.zeros((g["data"].shape[0], 77), np.uint8)])
+    _, _, ll3, _, _ = O.dense_tables(wide, g["arities"], queries, want_tables=False, m=g["data"].shape[1])
+    assert np.array_equal(ll, ll3)
+
+
+@pytest.mark.parametrize("n,m,density", [(3, 50, 0.5), (12, 3000, 0.3), (70, 20000, 0.05)])
+def test_itemset_enum_matches_bitmap_count(n, m, density):
+    import itertools
+
+    rng = np.random.default_rng(n * 1000 + m)
+    p = rng.uniform(0, 2 * density, n)
+    p[0] = 1.0  # an always-present item (cfg4's clipped p_1)
+    cols = (rng.random((n, m)) < p[:, None]).astype(np.uint8)
+    pairs, triples = O.itemset_supports_enum(cols, nthreads=3)
+    planes = {(v, 1): O.bitmap_planes(cols[v], 1) for v in range(n)}
+    combos2 = list(itertools.combinations(range(n), 2))
+    want2 = O.bitmap_counts(planes, [tuple((v, 1) for v in c) for c in combos2], m)
+    assert [int(pairs[a, b]) for a, b in combos2] == want2.tolist()
+    combos3 = list(itertools.combinations(range(n), 3))
+    want3 = O.bitmap_counts(planes, [tuple((v, 1) for v in c) for c in combos3], m)
+    assert triples.tolist() == want3.tolist()
+    for c in combos3[:: max(1, len(combos3) // 50)]:
+        assert O.oracle_count(cols, c, (1, 1, 1)) == triples[combos3.index(c)]
