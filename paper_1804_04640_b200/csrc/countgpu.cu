@@ -24,6 +24,7 @@
 #include "cs_radix.cuh"
 #include "cs_ingest.cuh"
 #include "cs_itemsets_sel.cuh"
+#include "cs_bitmapq.cuh"
 
 using namespace cs;
 
@@ -105,6 +106,12 @@ using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
 static const RadixPartFn kRadixPart[CS_MAXK] = {nullptr,         k_radix_part<2>, k_radix_part<3>,
                                                 k_radix_part<4>, k_radix_part<5>, k_radix_part<6>,
                                                 k_radix_part<7>, k_radix_part<8>};
+
+// K7 bitmap class per digit count
+using BitmapQFn = void (*)(const BDesc*, const BItem*, int, int*, int64_t, uint32_t*);
+static const BitmapQFn kBitmapQ[BQ_MAXK] = {k_bitmap_query<1>, k_bitmap_query<2>, k_bitmap_query<3>,
+                                            k_bitmap_query<4>};
+static int bq_smem_bytes(int k) { return BQ_STAGES * k * BQ_TILE * 4; }
 
 static int hist_path(const QDesc& d) {
   if (d.pack == 4) return P_PACK4;
@@ -242,6 +249,15 @@ struct cs_plan {
     int key, first, count;
   };
   std::vector<Group> groups;  // SMEM-class item groups, one K1 launch each
+  // kind 5 (bitmap class, cs_bitmapq.cuh): descriptors grouped by digit count, one launch per group
+  struct BLaunch {
+    int k, item0, nitems;
+  };
+  std::vector<BDesc> bdesc;
+  std::vector<BLaunch> blaunch;
+  BDesc* d_bdesc = nullptr;
+  BItem* d_bitems = nullptr;
+  int* d_bhead = nullptr;
   int nitems = 0;   // SMEM-class items (k_hist)
   int ngitems = 0;  // global-class items (k_hist_global), stored after the SMEM items
   // device
@@ -332,6 +348,9 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   for (RadixPartFn f : kRadixPart)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
+  for (int k = 1; k <= BQ_MAXK; ++k)
+    CS_CUDA(cudaFuncSetAttribute((const void*)kBitmapQ[k - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 bq_smem_bytes(k)));
   {  // keep freed ingest scratch in the device's stream-ordered pool between loads
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1120,6 +1139,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_nibble = env_int("CS_NIBBLE", 1) != 0;
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const bool knob_radix = env_int("CS_RADIX", 1) != 0;
+  // bitmap class (K7): -1 auto (cost model), 0 never, 1 whenever a query is eligible
+  const int knob_bitmap = env_int("CS_BITMAP", -1);
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
   // classification of every query (independent per query)
   const double trs = now_ms();
@@ -1162,8 +1183,20 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     d.nbyte = std::max(nbyte, 1);
     d.mode = c <= 65536 ? 1 : 2;
     d.r_target = db->arity[vars[b]];
+    // bitmap class: every digit binary with a state-1 plane, <= 4 digits.  Cost model (DESIGN.md
+    // K7): the planes are half the bytes of the 2-bit column copy and a word of 32 records costs
+    // 2^k - 1 POPC, so up to 3 digits it beats the histogram classes; 4 digits only when the
+    // database has no 2-bit copy (its histogram would read 4-bit columns)
+    bool bitmap_ok = knob_bitmap != 0 && !sparse && db->planes && k <= BQ_MAXK;
+    for (int i = 0; i < k && bitmap_ok; ++i) {
+      const int v = vars[b + i];
+      bitmap_ok = db->arity[v] == 2 && db->plane_off[v] >= 0;
+    }
+    if (bitmap_ok && knob_bitmap < 0) bitmap_ok = k <= 3 || !db->crumb;
     if (sparse) {
       d.kind = 3;  // hash class: descriptor built in the serial pass below
+    } else if (bitmap_ok) {
+      d.kind = 5;  // bitmap class: descriptor built in the serial pass below
     } else if (k > CS_MAXK) {
       d.kind = 2;  // generic class: variable list appended in the serial pass below
     } else if (c <= 6 && c * c * c * c * 32 <= smem_words && knob_pack) {
@@ -1320,6 +1353,14 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       sq.H = H;
       p->sparse.push_back(sq);
       p->cells[q] = 0;  // no dense table
+    } else if (d.kind == 5) {
+      BDesc bq;
+      memset(&bq, 0, sizeof bq);
+      for (int i = 0; i < k; ++i) bq.plane[i] = db->planes + db->plane_off[vars[b + i]] + db->words;
+      bq.table_off = total;
+      bq.k = k;
+      d.var_base = (int32_t)p->bdesc.size();  // BDesc index
+      p->bdesc.push_back(bq);
     } else if (d.kind == 2) {
       d.var_base = (int32_t)gvars.size();
       int64_t s2 = 1;
@@ -1348,7 +1389,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.nseg = 1;
       continue;
     }
-    if (d.kind == 4) {
+    if (d.kind == 4 || d.kind == 5) {
       p->score_list.push_back(q);
       p->needs_global = p->needs_zero = true;
       d.nseg = 1;
@@ -1554,7 +1595,31 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
     }
   }
+  // bitmap class (kind 5): (query, tile range) items grouped by digit count
+  std::vector<BItem> bitems;
+  if (!p->bdesc.empty()) {
+    const int64_t tiles = (db->words + BQ_TILE - 1) / BQ_TILE;
+    for (int k = 1; k <= BQ_MAXK; ++k) {
+      int64_t nqk = 0;
+      for (const BDesc& x : p->bdesc) nqk += x.k == k;
+      if (!nqk) continue;
+      // ~4 items per CTA of the launch, <= 16 tiles (512K records) each
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(16, nqk * tiles / (4LL * ctx->num_sms)));
+      cs_plan::BLaunch L{k, (int)bitems.size(), 0};
+      for (size_t i = 0; i < p->bdesc.size(); ++i) {
+        if (p->bdesc[i].k != k) continue;
+        for (int64_t t0 = 0; t0 < tiles; t0 += per)
+          bitems.push_back(BItem{(int32_t)i, (int32_t)t0, (int32_t)std::min(tiles, t0 + per)});
+      }
+      L.nitems = (int)bitems.size() - L.item0;
+      p->blaunch.push_back(L);
+    }
+  }
   const double tr2 = trace ? now_ms() : 0.0;
+  if (trace)
+    fprintf(stderr, "plan_build: classes smem=%lld global=%lld generic=%lld hash=%lld partition=%lld bitmap=%lld\n",
+            (long long)nkind[0], (long long)nkind[1], (long long)nkind[2], (long long)nkind[3], (long long)nkind[4],
+            (long long)nkind[5]);
   if (trace)
     fprintf(stderr, "plan_build: setup %.3f ms, classify %.3f ms (parallel part %.3f), items %.3f ms, order %.3f ms\n",
             trs - trc, tr0 - trs, trp - trs, tr1 - tr0,
@@ -1577,7 +1642,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
                ost = place(bst), oh = place(1024), od = place(sizeof(uint32_t) * std::max(nq, 1)),
                ord = place(sizeof(RDesc) * std::max<size_t>(p->rdesc.size(), 1)),
                ori = place(sizeof(RItem) * std::max<size_t>(ritems.size(), 1)),
-               orh = place(sizeof(int) * std::max<size_t>(p->waves.size(), 1));
+               orh = place(sizeof(int) * std::max<size_t>(p->waves.size(), 1)),
+               obd = place(sizeof(BDesc) * std::max<size_t>(p->bdesc.size(), 1)),
+               obi = place(sizeof(BItem) * std::max<size_t>(bitems.size(), 1)),
+               obh = place(sizeof(int) * BQ_MAXK);
   char* dblob = nullptr;
   p->transient = transient;
   if (transient) {
@@ -1615,9 +1683,13 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   memcpy(hs + ost, gstride.data(), sizeof(uint32_t) * gstride.size());
   memcpy(hs + ord, p->rdesc.data(), sizeof(RDesc) * p->rdesc.size());
   memcpy(hs + ori, ritems.data(), sizeof(RItem) * ritems.size());
+  memcpy(hs + obd, p->bdesc.data(), sizeof(BDesc) * p->bdesc.size());
+  memcpy(hs + obi, bitems.data(), sizeof(BItem) * bitems.size());
   CS_CUDA(cudaMemcpyAsync(dblob, hs, oh, cudaMemcpyHostToDevice, ctx->stream));
   if (!p->rdesc.empty())
     CS_CUDA(cudaMemcpyAsync(dblob + ord, hs + ord, orh - ord, cudaMemcpyHostToDevice, ctx->stream));
+  if (!p->bdesc.empty())
+    CS_CUDA(cudaMemcpyAsync(dblob + obd, hs + obd, obh - obd, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->pipe) {
     auto& ev = ctx->stage_ev[ctx->bank];
     if (!ev) CS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1635,6 +1707,9 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   p->d_rdesc = (RDesc*)(dblob + ord);
   p->d_ritems = (RItem*)(dblob + ori);
   p->d_rhead = (int*)(dblob + orh);
+  p->d_bdesc = (BDesc*)(dblob + obd);
+  p->d_bitems = (BItem*)(dblob + obi);
+  p->d_bhead = (int*)(dblob + obh);
   if (trace) fprintf(stderr, "plan_build: upload %.3f ms\n", now_ms() - tr2);
   *out = p;
   return CS_OK;
@@ -1988,6 +2063,23 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
         CS_CUDA(cudaGetLastError());
       }
     }
+  }
+  if (!p->blaunch.empty()) {
+    // bitmap class: subset popcounts per digit count, then the in-place superset -> cell transform
+    CS_CUDA(cudaMemsetAsync(p->d_bhead, 0, sizeof(int) * BQ_MAXK, ctx->stream));
+    for (size_t i = 0; i < p->blaunch.size(); ++i) {
+      const auto& L = p->blaunch[i];
+      const int per_sm = bq_smem_bytes(L.k) <= 100 * 1024 ? 2 : 1;
+      const int grid = std::min(L.nitems, per_sm * ctx->num_sms);
+      kBitmapQ[L.k - 1]<<<grid, BQ_THREADS, bq_smem_bytes(L.k), ctx->stream>>>(
+          p->d_bdesc, p->d_bitems + L.item0, L.nitems, p->d_bhead + i, db->words, dtab);
+      ctx->launches++;
+      CS_CUDA(cudaGetLastError());
+    }
+    const int nb = (int)p->bdesc.size();
+    k_bitmap_mobius<<<(nb + 127) / 128, 128, 0, ctx->stream>>>(p->d_bdesc, nb, (uint32_t)db->m, dtab);
+    ctx->launches++;
+    CS_CUDA(cudaGetLastError());
   }
   for (auto& sq : p->sparse) CS_TRY(run_sparse(p, sq, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
