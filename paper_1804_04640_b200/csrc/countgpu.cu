@@ -1183,16 +1183,15 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     d.nbyte = std::max(nbyte, 1);
     d.mode = c <= 65536 ? 1 : 2;
     d.r_target = db->arity[vars[b]];
-    // bitmap class: every digit binary with a state-1 plane, <= 4 digits.  Cost model (DESIGN.md
-    // K7): the planes are half the bytes of the 2-bit column copy and a word of 32 records costs
-    // 2^k - 1 POPC, so up to 3 digits it beats the histogram classes; 4 digits only when the
-    // database has no 2-bit copy (its histogram would read 4-bit columns)
+    // bitmap class: every digit binary with a state-1 plane, <= 4 digits.  The planes are half
+    // the bytes of the 2-bit column copy and a word of 32 records costs 2^k - 1 POPC, no SMEM
+    // atomics: measured 2.1-2.8x the histogram classes for k = 1..4 (tools/bitmap_compare.py,
+    // profiles/r02/bitmap_compare.txt), so every eligible query takes it
     bool bitmap_ok = knob_bitmap != 0 && !sparse && db->planes && k <= BQ_MAXK;
     for (int i = 0; i < k && bitmap_ok; ++i) {
       const int v = vars[b + i];
       bitmap_ok = db->arity[v] == 2 && db->plane_off[v] >= 0;
     }
-    if (bitmap_ok && knob_bitmap < 0) bitmap_ok = k <= 3 || !db->crumb;
     if (sparse) {
       d.kind = 3;  // hash class: descriptor built in the serial pass below
     } else if (bitmap_ok) {

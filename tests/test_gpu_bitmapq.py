@@ -82,7 +82,7 @@ def test_bitmap_class_mixed_batch_and_records(ctx, monkeypatch, capfd, reference
                 assert got == golden_records(q)
     rng = np.random.default_rng(5)
     n, m = 10, 200_000
-    ar = [2, 2, 2, 2, 2, 3, 4, 2, 5, 2]
+    ar = [2, 2, 2, 2, 2, 3, 4, 2, 5, 2]  # 5-ary variable: no 2-bit column copy
     data = np.vstack([rng.integers(0, a, m) for a in ar]).astype(np.uint8)
     gdb = GpuDatabase.from_columns(ctx, data, ar)
     gdb.bitmap_build()

@@ -78,7 +78,8 @@ def test_cfg2_all_bench_tables(ctx):
             assert np.array_equal(gdb.download(v), cols[v]), v
         plan = QueryPlan(gdb, w.queries, CS_WANT_TABLES)
         dev = torch.empty(max(plan.total_cells, 1), dtype=torch.int32, device="cuda")
-        plan.execute(tables=dev)  # the bench's timed step
+        plan.execute(tables=dev)  # the bench's timed step (asynchronous on the context stream)
+        ctx.sync()
         got = dev.cpu().numpy().view(np.uint32)[: plan.total_cells]
         otabs, ooff, _, _ = O.radix_tables(cols, w.arities, w.queries, nthreads=NT)
         assert np.array_equal(plan.table_off, ooff)
@@ -244,6 +245,7 @@ def test_cfg5_full_m(ctx):
             plan = QueryPlan(gdb, qs, CS_WANT_TABLES)
             dev = torch.empty(plan.total_cells, dtype=torch.int32, device="cuda")
             plan.execute(tables=dev)
+            ctx.sync()  # device outputs: the call is asynchronous on the context stream
             cs_ = torch.cumsum(dev.to(torch.int64), 0)
             ends = torch.from_numpy(plan.table_off + plan.cells - 1).cuda()
             starts = torch.from_numpy(plan.table_off).cuda()

@@ -27,6 +27,7 @@ def sums(qs):
     plan = QueryPlan(gdb, qs, CS_WANT_TABLES)
     dev = torch.empty(plan.total_cells, dtype=torch.int32, device="cuda")
     plan.execute(tables=dev)
+    ctx.sync()
     c = torch.cumsum(dev.to(torch.int64), 0).cpu().numpy()
     ends = plan.table_off + plan.cells - 1
     st = np.where(plan.table_off > 0, c[np.maximum(plan.table_off - 1, 0)], 0)
