@@ -589,6 +589,72 @@ class ItemsetRunner:
 
 
 # ---------------------------------------------------------------------------------------------
+# per-query drop-in latency (reference harness.py:222-275: bench_random times Strategy.query
+# one call at a time)
+
+
+def _per_query_us(strategy, queries, make_agg, reps=1):
+    for q in queries[:50]:  # warm-up (compiles / allocates outside the timed calls)
+        strategy.query(q, make_agg(q))
+    dts = []
+    for _ in range(reps):
+        for q in queries:
+            agg = make_agg(q)
+            t0 = time.perf_counter()
+            strategy.query(q, agg)
+            dts.append((time.perf_counter() - t0) * 1e6)
+            agg.result()
+    a = np.asarray(dts)
+    return {"mean_us": float(a.mean()), "p50_us": float(np.median(a)), "p99_us": float(np.percentile(a, 99)),
+            "queries_per_s": 1e6 / float(a.mean()), "calls": len(dts)}
+
+
+def dropin_ours() -> dict:
+    """cfg1's 1,000 queries, one GpuStrategy.query call each (built by make_strategies, the
+    reference's registry API), with the aggregators the reference's own benchmark and scorers use."""
+    import paper_1804_04640_b200 as cs
+    from paper_1804_04640_b200 import workloads as W
+
+    w = W.cfg1()
+    built, _ = cs.make_strategies(w.host_db, ("gpu",))
+    s = built["gpu"]
+    qs = [cs.QuerySpec(q[0], tuple(q[1:])) for q in w.queries]
+    out = {"workload": "cfg1 (n=20, m=1e4, 1,000 queries of target + 2 parents)",
+           "strategy": "gpu (GpuStrategy.query, one call per query)",
+           "NullSink": _per_query_us(s, qs, lambda q: cs.NullSink()),
+           "LogLikelihood": _per_query_us(s, qs, lambda q: cs.LogLikelihood()),
+           "RecordCollector": _per_query_us(s, qs, lambda q: cs.RecordCollector())}
+    return out
+
+
+def dropin_reference() -> dict:
+    """The same calls through the reference's own strategies (baseline/_ref, one core)."""
+    import tempfile
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "countstream").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_ref_"))
+    sys.path.insert(0, str(ref))
+    try:
+        import countstream as R
+    finally:
+        sys.path.remove(str(ref))
+    from paper_1804_04640_b200 import workloads as W
+
+    w = W.cfg1()
+    db = R.Database(w.host_db.data, [int(a) for a in w.arities])
+    built, _ = R.make_strategies(db, ("bitmap", "radix"))
+    qs = [R.QuerySpec(q[0], tuple(q[1:])) for q in w.queries]
+    out = {"workload": "cfg1 (n=20, m=1e4, 1,000 queries of target + 2 parents)"}
+    for name in ("bitmap", "radix"):
+        out[name] = {"NullSink": _per_query_us(built[name], qs, lambda q: R.NullSink()),
+                     "LogLikelihood": _per_query_us(built[name], qs, lambda q: R.LogLikelihood()),
+                     "RecordCollector": _per_query_us(built[name], qs, lambda q: R.RecordCollector())}
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
 # arms
 
 
@@ -708,6 +774,9 @@ def run_reference(args, world, rank):
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "native_engine_loaded": _engine_loaded(),
     }
+    if args.config == "cfg2" and not args.no_dropin:
+        line["dropin"] = dropin_reference()
+        line["native_engine_loaded"] = _engine_loaded()
     print(json.dumps(line), flush=True)
 
 
@@ -804,6 +873,8 @@ def run_ours(args, world, rank, local):
         "diag": {"step_ms": [round(x, 4) for x in ms[:8]]},
         "clocks": clk.summary(),
     }
+    if rank == 0 and world == 1 and args.config == "cfg2" and not args.no_dropin:
+        line["dropin"] = dropin_ours()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, desc = r.cpu_baseline(args.ref_budget, threads)
@@ -828,6 +899,7 @@ def main():
     ap.add_argument("--m", type=int, default=None, help="rows (cfg4 only; default 1e7)")
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the per-query drop-in latency block")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

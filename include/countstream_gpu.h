@@ -185,6 +185,15 @@ int cs_plan_destroy(cs_plan* plan);
 int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t* vars,
                    uint32_t flags, uint32_t* tables, double* loglik, double* mi, int64_t* nnz);
 
+/* One query with the lowest latency (the drop-in Strategy.query path; replaces one
+ * radix_query / bitmap_query call, radix.py:113-156, bitmap.py:69-128).  vars: host int32[k],
+ * target first.  Outputs as cs_query_batch for nq = 1 (any may be NULL).  Small queries (k <= 8,
+ * <= 49,152 cells, m <= 2^18 rows; env CS_ONE_MAX_ROWS) run as one kernel whose descriptor is a
+ * launch parameter and whose results land in mapped host memory; anything else goes through
+ * cs_query_batch.  Synchronous. */
+int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table, double* loglik,
+                 double* mi, int64_t* nnz);
+
 /* Batched MDL parent-set scoring (learn_parents, harness.py:296-348; MdlScore,
  * aggregators.py:163-193).  nlogn[nsub]: CS_NLOGN outputs of a plan over the distinct variable
  * subsets; family f scores  ll[f] = nlogn[s_idx[f]] - (p_idx[f] >= 0 ? nlogn[p_idx[f]] : m_ln_m)

@@ -68,6 +68,7 @@ SIGNATURES = [
     ("cs_plan_destroy", c_int, [_P]),
     ("cs_family_scores", c_int, [_P, c_int64, _P, c_int64, _P, _P, _P, c_double, _P, _P]),
     ("cs_query_batch", c_int, [_P, c_int32, _P, _P, c_uint32, _P, _P, _P, _P]),
+    ("cs_query_one", c_int, [_P, c_int32, _P, c_uint32, _P, _P, _P, _P]),
     ("cs_count_points", c_int, [_P, c_int32, _P, _P, _P, _P]),
     ("cs_itemset_supports", c_int, [_P, c_int32, _P, _P, _P]),
 ]

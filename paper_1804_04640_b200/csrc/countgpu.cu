@@ -25,6 +25,7 @@
 #include "cs_ingest.cuh"
 #include "cs_itemsets_sel.cuh"
 #include "cs_bitmapq.cuh"
+#include "cs_one.cuh"
 
 using namespace cs;
 
@@ -155,6 +156,10 @@ struct cs_ctx {
   size_t pinned1_bytes = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   bool stage_ev_valid[2] = {false, false};
+  // cs_query_one mailbox: page-locked, device-mapped host memory the K8 kernel stores into
+  // (3 scalars, then up to ONE_MAX_CELLS table cells)
+  char* mbox = nullptr;
+  char* mbox_dev = nullptr;
 
   int scratch_get(int slot, size_t bytes, void** out) {
     auto& s = scratch[slot + 1000 * bank];
@@ -348,6 +353,8 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   for (RadixPartFn f : kRadixPart)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_query_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(ONE_MAX_CELLS * 4)));
   for (int k = 1; k <= BQ_MAXK; ++k)
     CS_CUDA(cudaFuncSetAttribute((const void*)kBitmapQ[k - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  bq_smem_bytes(k)));
@@ -385,6 +392,7 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
     if (kv.second.first) cudaFree(kv.second.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned1) cudaFreeHost(ctx->pinned1);
+  if (ctx->mbox) cudaFreeHost(ctx->mbox);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -2300,6 +2308,74 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
   cs_plan_destroy(p);
   if (trace) fprintf(stderr, "cs_query_batch: plan %.3f ms, execute+copy %.3f ms\n", t1 - t0, t2 - t1);
   return rc;
+}
+
+// one query, latency class (K8, cs_one.cuh)
+extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table,
+                            double* loglik, double* mi, int64_t* nnz) {
+  CtxLock lk_(db ? db->ctx : nullptr);
+  if (!db) return fail(CS_ERR_INVALID, "cs_query_one: NULL db");
+  if (k < 1) return fail(CS_ERR_INVALID, "query 0 has no target variable");
+  if (!vars) return fail(CS_ERR_INVALID, "cs_query_one: vars is NULL");
+  uint64_t C = 1;
+  for (int i = 0; i < k; ++i) {
+    const int v = vars[i];
+    if (v < 0 || v >= db->n) return fail(CS_ERR_INVALID, "variable %d out of range for a database with n=%d", v, db->n);
+    for (int j = 0; j < i; ++j)
+      if (vars[j] == v) return fail(CS_ERR_INVALID, "query 0 repeats variable %d", v);
+    if (C > (((uint64_t)1 << 63) - 1) / (uint64_t)db->arity[v])
+      return fail(CS_ERR_UNSUPPORTED, "query 0: joint state space exceeds 2^63 cells");
+    C *= (uint64_t)db->arity[v];
+  }
+  const int64_t max_rows = env_int("CS_ONE_MAX_ROWS", 1 << 18);
+  const bool one = k <= CS_MAXK && C <= ONE_MAX_CELLS && db->m <= max_rows && !(flags & (F_PARTIAL | F_NLOGN)) &&
+                   env_int("CS_ONE", 1) != 0;
+  if (!one) {  // the batch path (transient plan) answers everything else
+    const int32_t off[2] = {0, k};
+    return cs_query_batch(db, 1, off, vars, flags, table, loglik, mi, nnz);
+  }
+  cs_ctx* ctx = db->ctx;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (!ctx->mbox) {
+    CS_CUDA(cudaHostAlloc((void**)&ctx->mbox, 64 + (size_t)ONE_MAX_CELLS * 4, cudaHostAllocMapped));
+    CS_CUDA(cudaHostGetDevicePointer((void**)&ctx->mbox_dev, ctx->mbox, 0));
+  }
+  OneQ q;
+  memset(&q, 0, sizeof q);
+  uint32_t s = 1;
+  for (int i = 0; i < k; ++i) {
+    q.col[i] = db->cols + (int64_t)vars[i] * db->ld;
+    q.stride[i] = s;
+    s *= (uint32_t)db->arity[vars[i]];
+  }
+  q.k = k;
+  q.r_t = db->arity[vars[0]];
+  q.cells = (uint32_t)C;
+  q.flags = flags | (loglik ? F_LOGLIK : 0u) | (mi ? F_MI : 0u) | (nnz ? F_NNZ : 0u);
+  q.m = db->m;
+  q.m_total = (double)db->m_total;
+  const bool table_dev = table && is_device_ptr(table);
+  q.table = table ? (table_dev ? table : (uint32_t*)(ctx->mbox_dev + 64)) : nullptr;
+  q.out = (double*)ctx->mbox_dev;
+  k_query_one<<<1, ONE_THREADS, (size_t)C * 4, ctx->stream>>>(q);
+  ctx->launches++;
+  CS_CUDA(cudaGetLastError());
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double* o = (const double*)ctx->mbox;
+  auto put = [&](void* user, const void* src, size_t bytes) -> int {
+    if (!user) return CS_OK;
+    if (is_device_ptr(user)) {
+      CS_CUDA(cudaMemcpy(user, src, bytes, cudaMemcpyHostToDevice));
+    } else {
+      memcpy(user, src, bytes);
+    }
+    return CS_OK;
+  };
+  CS_TRY(put(loglik, o, 8));
+  CS_TRY(put(mi, o + 1, 8));
+  CS_TRY(put(nnz, o + 2, 8));
+  if (table && !table_dev) memcpy(table, ctx->mbox + 64, (size_t)C * 4);
+  return CS_OK;
 }
 
 // ------------------------------------------------------------------------------------------

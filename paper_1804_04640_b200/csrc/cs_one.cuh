@@ -1,0 +1,62 @@
+// cs_one.cuh -- K8, the single-query latency class behind cs_query_one (the drop-in
+// Strategy.query path: reference radix.py:113-156 / bitmap.py:69-128 answer one query per
+// call, and harness.py:222-275 times exactly that).
+//
+// A batch plan costs a descriptor upload, several launches and a device sync; for one small
+// query that fixed cost dwarfs the counting.  Here the whole query travels as a kernel
+// parameter (no upload), one CTA counts every row into an SMEM table, scores it with the
+// shared fp64 epilogue (score_table) and stores the results -- scalars and, when asked, the
+// dense table -- straight into page-locked, device-mapped host memory: one launch and one
+// stream sync per query.
+#pragma once
+#include <cstdint>
+
+#include "cs_common.cuh"
+#include "cs_kernels.cuh"
+
+namespace cs {
+
+constexpr int ONE_THREADS = 1024;
+constexpr uint32_t ONE_MAX_CELLS = 48 * 1024;  // 192 KB of SMEM counters
+
+struct OneQ {
+  const uint8_t* col[CS_MAXK];  // uint8 column of digit v (target first)
+  uint32_t stride[CS_MAXK];
+  int32_t k, r_t;
+  uint32_t cells;
+  uint32_t flags;
+  int64_t m;
+  double m_total;
+  uint32_t* table;  // mapped host (or device) dense table, or NULL
+  double* out;      // [0] LL, [1] MI, [2] nnz (int64 bits)
+};
+
+__global__ void __launch_bounds__(ONE_THREADS, 1) k_query_one(const OneQ q) {
+  extern __shared__ __align__(16) uint32_t one_tab[];
+  __shared__ ScoreSmem ss;
+  const int tid = threadIdx.x;
+  for (uint32_t c = tid; c < q.cells; c += ONE_THREADS) one_tab[c] = 0;
+  __syncthreads();
+  // 4 rows per thread step: one 32-bit load per column (columns are 256-B aligned and padded)
+  for (int64_t r0 = (int64_t)tid * 4; r0 < q.m; r0 += 4 * ONE_THREADS) {
+    uint32_t idx[4] = {0, 0, 0, 0};
+    for (int v = 0; v < q.k; ++v) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(q.col[v] + r0));
+      const uint32_t s = q.stride[v];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) idx[r] += ((w >> (8 * r)) & 0xffu) * s;
+    }
+    const int nr = q.m - r0 >= 4 ? 4 : (int)(q.m - r0);
+    for (int r = 0; r < nr; ++r) atomicAdd(&one_tab[idx[r]], 1u);
+  }
+  __syncthreads();
+  if (q.table)
+    for (uint32_t c = tid; c < q.cells; c += ONE_THREADS) q.table[c] = one_tab[c];
+  if (q.flags & (F_LOGLIK | F_MI | F_NNZ)) {
+    auto cell = [&](uint32_t c) { return one_tab[c]; };
+    score_table(cell, q.cells, q.r_t, q.m_total, q.flags, 0, q.out, q.out + 1,
+                reinterpret_cast<int64_t*>(q.out + 2), ss);
+  }
+}
+
+}  // namespace cs

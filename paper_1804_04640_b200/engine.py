@@ -246,6 +246,11 @@ class GpuDatabase:
         check(lib.cs_query_batch(self._h, len(var_off) - 1, ptr(var_off), ptr(vars_), int(flags),
                                  ptr(tables), ptr(loglik), ptr(mi), ptr(nnz)))
 
+    def query_one(self, vars_: np.ndarray, flags: int = 0, tables=None, loglik=None, mi=None, nnz=None) -> None:
+        """One query (int32 variables, target first) through cs_query_one (latency class)."""
+        check(lib.cs_query_one(self._h, len(vars_), ptr(vars_), int(flags), ptr(tables), ptr(loglik), ptr(mi),
+                               ptr(nnz)))
+
     def count_points(self, assignments) -> np.ndarray:
         """assignments: iterable of (variables, states) pairs -> int64 counts."""
         assignments = list(assignments)

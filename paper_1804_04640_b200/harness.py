@@ -198,24 +198,45 @@ class GpuStrategy(Strategy):
             self.gdb.bitmap_build()
 
     # -- drop-in per-query API ------------------------------------------------------------
+    #: dense tables up to this many cells come back whole and are compacted on the host (one
+    #: engine call); larger ones are compacted on the device (K5) through a plan
+    HOST_COMPACT_CELLS = 1 << 16
+
     def query(self, q: QuerySpec, agg) -> None:
+        """One query through cs_query_one (K8 latency class: one launch, descriptor as a kernel
+        parameter, results in mapped host memory; larger queries take the one-shot batch path
+        inside the library): fused scalars for NullSink / LogLikelihood / MdlScore /
+        MutualInformation, the dense table compacted on the host for small tables, the K5
+        device compaction otherwise."""
         q.validate(self.db)
         kind = _fusion_kind(agg)
-        with self._lock:
-            if kind is not None:
-                plan = QueryPlan(self.gdb, [_vars(q)])
-                ll = np.zeros(1)
-                mi = np.zeros(1)
+        vs = _vars(q)
+        flat = np.array(vs, dtype=np.int32)
+        ar = self.gdb.arities
+        if kind is not None:
+            out = np.zeros(3)  # ll, mi, nnz
+            self.gdb.query_one(flat, 0, loglik=out[0:1], mi=out[1:2] if kind == "mi" else None,
+                               nnz=out[2:3].view(np.int64))
+            _absorb(agg, kind, float(out[0]), float(out[1]), int(out[2:3].view(np.int64)[0]))
+            return
+        cells = 1
+        for v in vs:
+            cells *= int(ar[v])
+        if cells <= self.HOST_COMPACT_CELLS:
+            tab = np.zeros(cells, dtype=np.uint32)
+            self.gdb.query_one(flat, N.CS_WANT_TABLES, tables=tab)
+            r_t = int(ar[vs[0]])
+            nij_all = tab.reshape(-1, r_t).sum(axis=1, dtype=np.int64)
+            cidx = np.flatnonzero(tab)
+            nijk = tab[cidx].astype(np.int64)
+            nij = nij_all[cidx // r_t]
+        else:
+            with self._lock:
+                plan = QueryPlan(self.gdb, [vs], N.CS_WANT_TABLES)
                 nnz = np.zeros(1, dtype=np.int64)
-                plan.execute(loglik=ll, mi=mi if kind == "mi" else None, nnz=nnz)
+                plan.execute(nnz=nnz)
+                _, cidx, nijk, nij = plan.compact(None, nnz)
                 plan.close()
-                _absorb(agg, kind, float(ll[0]), float(mi[0]), int(nnz[0]))
-                return
-            plan = QueryPlan(self.gdb, [_vars(q)], N.CS_WANT_TABLES)
-            nnz = np.zeros(1, dtype=np.int64)
-            plan.execute(nnz=nnz)
-            _, cidx, nijk, nij = plan.compact(None, nnz)
-            plan.close()
         self._deliver(q, agg, cidx, nijk, nij)
 
     def _deliver(self, q: QuerySpec, agg, cidx, nijk, nij) -> None:
@@ -252,19 +273,19 @@ class GpuStrategy(Strategy):
         ``table_off`` are None; with ``tables`` a QueryPlan also reports each table's layout.
         """
         qs = list(queries)
-        for q in qs:
-            q.validate(self.db)
+        enc = _encode_specs(qs) if qs else None
+        self._validate_encoded(qs, enc)
         if not tables:
             ll = np.zeros(len(qs)) if loglik else None
             mv = np.zeros(len(qs)) if mi else None
             nz = np.zeros(len(qs), dtype=np.int64) if nnz else None
             if qs:
-                off, flat = _encode_specs(qs)
+                off, flat = enc
                 with self._lock:
                     self.gdb.query_batch(off, flat, 0, loglik=ll, mi=mv, nnz=nz)
             return {"loglik": ll, "mi": mv, "nnz": nz, "tables": None, "cells": None, "table_off": None}
         with self._lock:
-            plan = QueryPlan(self.gdb, _encode_specs(qs), N.CS_WANT_TABLES if tables else 0)
+            plan = QueryPlan(self.gdb, enc if qs else [], N.CS_WANT_TABLES if tables else 0)
             out = {}
             ll = np.zeros(len(qs)) if loglik else None
             mv = np.zeros(len(qs)) if mi else None
@@ -276,6 +297,16 @@ class GpuStrategy(Strategy):
                         "cells": plan.cells, "table_off": plan.table_off})
             plan.close()
         return out
+
+    def _validate_encoded(self, qs, enc) -> None:
+        """QuerySpec.validate (variable < n; construction already checked the rest) for a whole
+        batch with one vectorised test; on failure the per-query loop raises the reference's
+        error for the first offending query."""
+        if enc is None:
+            return
+        if len(enc[1]) and int(enc[1].max()) >= self.db.n:
+            for q in qs:
+                q.validate(self.db)
 
     def family_scores(self, families) -> tuple[np.ndarray, np.ndarray]:
         """(LL, MDL) of many (target, parents) families from one launch over their distinct
