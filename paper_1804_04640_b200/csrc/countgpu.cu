@@ -4,6 +4,7 @@
 // query gets) happens here on the host in C++; the hot loops are the kernels in
 // cs_kernels.cuh.  See DESIGN.md for the kernel classes and their rooflines.
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -160,6 +161,7 @@ struct cs_ctx {
   // (3 scalars, then up to ONE_MAX_CELLS table cells)
   char* mbox = nullptr;
   char* mbox_dev = nullptr;
+  uint32_t one_seq = 0;
 
   int scratch_get(int slot, size_t bytes, void** out) {
     auto& s = scratch[slot + 1000 * bank];
@@ -2357,10 +2359,22 @@ extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t 
   const bool table_dev = table && is_device_ptr(table);
   q.table = table ? (table_dev ? table : (uint32_t*)(ctx->mbox_dev + 64)) : nullptr;
   q.out = (double*)ctx->mbox_dev;
+  q.done = (volatile uint32_t*)(ctx->mbox_dev + 32);
+  q.seq = ++ctx->one_seq;
+  volatile uint32_t* done = (volatile uint32_t*)(ctx->mbox + 32);
   k_query_one<<<1, ONE_THREADS, (size_t)C * 4, ctx->stream>>>(q);
   ctx->launches++;
   CS_CUDA(cudaGetLastError());
-  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  // poll the mapped completion word (a stream sync costs several microseconds more); after
+  // ~2 ms fall back to the stream sync, which also reports a failed kernel
+  const double t0 = now_ms();
+  bool seen = false;
+  for (int spin = 0; !seen; ++spin) {
+    seen = *done == q.seq;
+    if (!seen && (spin & 1023) == 1023 && now_ms() - t0 > 2.0) break;
+  }
+  if (!seen) CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::atomic_thread_fence(std::memory_order_acquire);
   const double* o = (const double*)ctx->mbox;
   auto put = [&](void* user, const void* src, size_t bytes) -> int {
     if (!user) return CS_OK;

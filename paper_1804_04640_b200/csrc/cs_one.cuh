@@ -29,6 +29,8 @@ struct OneQ {
   double m_total;
   uint32_t* table;  // mapped host (or device) dense table, or NULL
   double* out;      // [0] LL, [1] MI, [2] nnz (int64 bits)
+  volatile uint32_t* done;  // mapped host word: set to `seq` once every result above is visible
+  uint32_t seq;
 };
 
 __global__ void __launch_bounds__(ONE_THREADS, 1) k_query_one(const OneQ q) {
@@ -57,6 +59,11 @@ __global__ void __launch_bounds__(ONE_THREADS, 1) k_query_one(const OneQ q) {
     score_table(cell, q.cells, q.r_t, q.m_total, q.flags, 0, q.out, q.out + 1,
                 reinterpret_cast<int64_t*>(q.out + 2), ss);
   }
+  // completion word: the host polls it instead of a stream synchronisation (lower latency);
+  // every thread's stores are fenced to system scope before thread 0 publishes
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) *q.done = q.seq;
 }
 
 }  // namespace cs

@@ -170,6 +170,14 @@ def _absorb(agg, kind: str, ll: float, mi: float, nnz: int) -> None:
         raise TypeError(f"cannot fuse {type(agg)}")
 
 
+def _dense_limit() -> int:
+    """Largest joint state space the engine counts in a dense table (its CS_MAX_DENSE_LOG2
+    knob; larger ones go to the hash class, which has no dense table to return)."""
+    import os
+
+    return 1 << int(os.environ.get("CS_MAX_DENSE_LOG2", "30") or 30)
+
+
 class GpuStrategy(Strategy):
     """The B200 engine behind the reference's Strategy facade.
 
@@ -187,6 +195,7 @@ class GpuStrategy(Strategy):
         self.db = db
         self.ctx = shared_context(device)
         self._lock = threading.Lock()
+        self._tls = threading.local()
         if isinstance(db, DeviceDatabase):
             self.gdb = db.gdb
         else:
@@ -211,18 +220,25 @@ class GpuStrategy(Strategy):
         q.validate(self.db)
         kind = _fusion_kind(agg)
         vs = _vars(q)
-        flat = np.array(vs, dtype=np.int32)
         ar = self.gdb.arities
         if kind is not None:
-            out = np.zeros(3)  # ll, mi, nnz
-            self.gdb.query_one(flat, 0, loglik=out[0:1], mi=out[1:2] if kind == "mi" else None,
-                               nnz=out[2:3].view(np.int64))
-            _absorb(agg, kind, float(out[0]), float(out[1]), int(out[2:3].view(np.int64)[0]))
+            # per-thread scratch with cached addresses: no numpy / ctypes helper objects per call
+            sc = self._tls.__dict__.get("one")
+            if sc is None or len(sc[0]) < len(vs):
+                vb = np.zeros(max(64, len(vs)), dtype=np.int32)
+                ob = np.zeros(3)
+                sc = self._tls.one = (vb, ob, vb.ctypes.data, ob.ctypes.data)
+            vb, ob, va, oa = sc
+            vb[:len(vs)] = vs
+            N.check(N.lib.cs_query_one(self.gdb.handle, len(vs), va, 0, None, oa,
+                                       oa + 8 if kind == "mi" else None, oa + 16))
+            _absorb(agg, kind, float(ob[0]), float(ob[1]), int(ob[2:3].view(np.int64)[0]))
             return
+        flat = np.array(vs, dtype=np.int32)
         cells = 1
         for v in vs:
             cells *= int(ar[v])
-        if cells <= self.HOST_COMPACT_CELLS:
+        if cells <= min(self.HOST_COMPACT_CELLS, _dense_limit()):
             tab = np.zeros(cells, dtype=np.uint32)
             self.gdb.query_one(flat, N.CS_WANT_TABLES, tables=tab)
             r_t = int(ar[vs[0]])
