@@ -1152,6 +1152,16 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // bitmap class (K7): -1 auto (cost model), 0 never, 1 whenever a query is eligible
   const int knob_bitmap = env_int("CS_BITMAP", -1);
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
+  // tables above SMEM: the slice class (columns re-read once per pass, from L2) when it needs at
+  // most this many passes over a row segment, else the partition class
+  const int knob_slice_passes = env_int("CS_SLICE_MAX_PASSES", 0);
+  auto slice_passes = [&](int64_t c, int rlast) -> int64_t {
+    const int64_t sc = c / rlast;
+    int rl = 0;
+    while (rl < 5 && (sc << (rl + 1)) <= smem_words) ++rl;
+    const int64_t spc = std::max<int64_t>(1, smem_words / (sc << rl));
+    return (rlast + spc - 1) / spc;
+  };
   // classification of every query (independent per query)
   const double trs = now_ms();
   auto classify = [&](int q) -> int {
@@ -1244,7 +1254,9 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           d.rlog = rh;
         }
       }
-    } else if (knob_radix && db->nib && k >= 2 && c <= ((int64_t)1 << 24)) {
+    } else if (knob_radix && db->nib && k >= 2 && c <= ((int64_t)1 << 24) &&
+               !(knob_slice && c / db->arity[vars[e - 1]] <= smem_words &&
+                 slice_passes(c, db->arity[vars[e - 1]]) <= knob_slice_passes)) {
       // partition class (cs_radix.cuh): one counting-sort pass by the high bits of the joint
       // index, then SMEM histograms per 32K-cell group; reads the 4-bit columns
       d.kind = 4;

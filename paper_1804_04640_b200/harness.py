@@ -234,13 +234,22 @@ class GpuStrategy(Strategy):
                                        oa + 8 if kind == "mi" else None, oa + 16))
             _absorb(agg, kind, float(ob[0]), float(ob[1]), int(ob[2:3].view(np.int64)[0]))
             return
-        flat = np.array(vs, dtype=np.int32)
         cells = 1
         for v in vs:
             cells *= int(ar[v])
         if cells <= min(self.HOST_COMPACT_CELLS, _dense_limit()):
-            tab = np.zeros(cells, dtype=np.uint32)
-            self.gdb.query_one(flat, N.CS_WANT_TABLES, tables=tab)
+            tb = self._tls.__dict__.get("tab")
+            if tb is None:
+                buf = np.zeros(self.HOST_COMPACT_CELLS, dtype=np.uint32)
+                vb = np.zeros(64, dtype=np.int32)
+                tb = self._tls.tab = (buf, buf.ctypes.data, vb, vb.ctypes.data)
+            buf, ba, vb, va = tb
+            if len(vs) <= len(vb):
+                vb[:len(vs)] = vs
+                N.check(N.lib.cs_query_one(self.gdb.handle, len(vs), va, N.CS_WANT_TABLES, ba, None, None, None))
+            else:
+                self.gdb.query_one(np.array(vs, dtype=np.int32), N.CS_WANT_TABLES, tables=buf)
+            tab = buf[:cells]
             r_t = int(ar[vs[0]])
             nij_all = tab.reshape(-1, r_t).sum(axis=1, dtype=np.int64)
             cidx = np.flatnonzero(tab)
@@ -263,16 +272,18 @@ class GpuStrategy(Strategy):
         r_t = int(ar[q.target])
         radices = [int(ar[p]) for p in q.parents]
         order = sorted(range(len(q.parents)), key=lambda t: q.parents[t])
-        ks = cidx % r_t
-        js = cidx // r_t
-        for t in range(len(cidx)):
-            j = int(js[t])
+        ks = (cidx % r_t).tolist()
+        js = (cidx // r_t).tolist()
+        a, b = nijk.tolist(), nij.tolist()
+        parents = q.parents
+        accept = agg.accept_record
+        for t in range(len(js)):
+            j = js[t]
             states = []
             for r in radices:
                 j, s = divmod(j, r)
                 states.append(s)
-            config = tuple((q.parents[u], states[u]) for u in order)
-            agg.accept_record(config, int(ks[t]), int(nijk[t]), int(nij[t]))
+            accept(tuple((parents[u], states[u]) for u in order), ks[t], a[t], b[t])
 
     def count(self, a: Assignment) -> int:
         a.validate(self.db)
