@@ -108,6 +108,10 @@ using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
 static const RadixPartFn kRadixPart[CS_MAXK] = {nullptr,         k_radix_part<2>, k_radix_part<3>,
                                                 k_radix_part<4>, k_radix_part<5>, k_radix_part<6>,
                                                 k_radix_part<7>, k_radix_part<8>};
+// multisplit variant for tables of <= RX_MS_MAXG count groups
+static const RadixPartFn kRadixPartMS[CS_MAXK] = {nullptr,            k_radix_part_ms<2>, k_radix_part_ms<3>,
+                                                  k_radix_part_ms<4>, k_radix_part_ms<5>, k_radix_part_ms<6>,
+                                                  k_radix_part_ms<7>, k_radix_part_ms<8>};
 
 // K7 bitmap class per digit count
 using BitmapQFn = void (*)(const BDesc*, const BItem*, int, int*, int64_t, uint32_t*);
@@ -239,7 +243,8 @@ struct cs_plan {
   // kind 4 (partition class, cs_radix.cuh): queries in wave order, processed in waves whose
   // partition buffers share one context scratch (slot 23)
   struct RadixLaunch {
-    int k, first, count;  // k_radix_part<k> over RDescs [first, first + count)
+    int k, first, count;  // k_radix_part<k> (or _ms<k>) over RDescs [first, first + count)
+    bool ms;
   };
   struct RadixWave {
     std::vector<RadixLaunch> parts;
@@ -353,6 +358,8 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
                                                         c->hist_smem));
   if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
   for (RadixPartFn f : kRadixPart)
+    if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
+  for (RadixPartFn f : kRadixPartMS)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_query_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1555,7 +1562,13 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     for (int q = 0; q < nq; ++q)
       if (p->hq[q].kind == 4) rq.push_back(q);
     if (!rq.empty()) {
-      std::stable_sort(rq.begin(), rq.end(), [&](int a, int b) { return p->hq[a].k < p->hq[b].k; });
+      const bool knob_ms = env_int("CS_RADIX_MS", 1) != 0;
+      auto is_ms = [&](int q) {
+        return knob_ms && (((int64_t)p->hq[q].cells + (1LL << RX_GROUP_BITS) - 1) >> RX_GROUP_BITS) <= RX_MS_MAXG;
+      };
+      std::stable_sort(rq.begin(), rq.end(), [&](int a, int b) {
+        return p->hq[a].k != p->hq[b].k ? p->hq[a].k < p->hq[b].k : (int)is_ms(a) < (int)is_ms(b);
+      });
       const int64_t nchunks = (m + RX_CH - 1) / RX_CH;
       p->rx_nchunks = (int)nchunks;
       const size_t buf_b = (size_t)round_up(nchunks * RX_CH * 2, 256);
@@ -1584,8 +1597,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           r.q = q;
           r.base = d.base;
           const int64_t C = d.cells;
+          const bool ms = is_ms(q);
           int bb = 10;  // >= 32 buckets where possible (SMEM bucket counters contend less)
           while (bb < RX_GROUP_BITS && (C >> (bb + 1)) >= 32) ++bb;
+          if (ms) bb = RX_GROUP_BITS;  // multisplit: one bucket per count group
           r.bb = bb;
           r.nb = (int)((C + (1LL << bb) - 1) >> bb);
           {
@@ -1604,7 +1619,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           r.wlog = wl;
           const int ri = (int)p->rdesc.size();
           p->rdesc.push_back(r);
-          if (wave.parts.empty() || wave.parts.back().k != d.k) wave.parts.push_back({d.k, ri, 0});
+          if (wave.parts.empty() || wave.parts.back().k != d.k || wave.parts.back().ms != ms)
+            wave.parts.push_back({d.k, ri, 0, ms});
           wave.parts.back().count++;
           const int ngrp = (int)((C + (1LL << RX_GROUP_BITS) - 1) >> RX_GROUP_BITS);
           for (int g = 0; g < ngrp; ++g)
@@ -2071,8 +2087,8 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
         const int total = L.count * p->rx_nchunks;
         if (total == 0) continue;
         const int grid = std::min(total, 4 * ctx->num_sms);
-        kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(p->d_rdesc + L.first, L.count,
-                                                                         p->rx_nchunks, db->m, (char*)scr);
+        (L.ms ? kRadixPartMS : kRadixPart)[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(
+            p->d_rdesc + L.first, L.count, p->rx_nchunks, db->m, (char*)scr);
         ctx->launches++;
         CS_CUDA(cudaGetLastError());
       }
