@@ -97,8 +97,10 @@ using HistFn = void (*)(const QDesc*, const WItem*, int, int*, uint32_t*, uint32
    {K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 0> : nullptr,                               \
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 1> : nullptr,                               \
     K <= 5 ? k_hist<(K <= 5 ? K : 5), P_PACK4, 2> : nullptr},                              \
-   CS_HK3(K, P_ROWS), CS_HK3(K, P_HALF), CS_HK3(K, P_SLICE)}
-static const HistFn kHist[CS_MAXK][6][3] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
+   CS_HK3(K, P_ROWS), CS_HK3(K, P_HALF), CS_HK3(K, P_SLICE),                                \
+   {nullptr, K >= 2 ? k_hist<(K >= 2 ? K : 2), P_NARROW8, 1> : nullptr, nullptr},             \
+   {nullptr, K >= 2 ? k_hist<(K >= 2 ? K : 2), P_NARROW16, 1> : nullptr, nullptr}}
+static const HistFn kHist[CS_MAXK][8][3] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(4),
                                             CS_HK(5), CS_HK(6), CS_HK(7), CS_HK(8)};
 #undef CS_HK3
 #undef CS_HK
@@ -108,10 +110,6 @@ using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
 static const RadixPartFn kRadixPart[CS_MAXK] = {nullptr,         k_radix_part<2>, k_radix_part<3>,
                                                 k_radix_part<4>, k_radix_part<5>, k_radix_part<6>,
                                                 k_radix_part<7>, k_radix_part<8>};
-// multisplit variant for tables of <= RX_MS_MAXG count groups
-static const RadixPartFn kRadixPartMS[CS_MAXK] = {nullptr,            k_radix_part_ms<2>, k_radix_part_ms<3>,
-                                                  k_radix_part_ms<4>, k_radix_part_ms<5>, k_radix_part_ms<6>,
-                                                  k_radix_part_ms<7>, k_radix_part_ms<8>};
 
 // K7 bitmap class per digit count
 using BitmapQFn = void (*)(const BDesc*, const BItem*, int, int*, int64_t, uint32_t*);
@@ -120,6 +118,8 @@ static const BitmapQFn kBitmapQ[BQ_MAXK] = {k_bitmap_query<1>, k_bitmap_query<2>
 static int bq_smem_bytes(int k) { return BQ_STAGES * k * BQ_TILE * 4; }
 
 static int hist_path(const QDesc& d) {
+  if (d.narrow == 8) return P_NARROW8;
+  if (d.narrow == 16) return P_NARROW16;
   if (d.pack == 4) return P_PACK4;
   if (d.pack == 2) return P_PACK2;
   if (d.half) return P_HALF;
@@ -243,8 +243,7 @@ struct cs_plan {
   // kind 4 (partition class, cs_radix.cuh): queries in wave order, processed in waves whose
   // partition buffers share one context scratch (slot 23)
   struct RadixLaunch {
-    int k, first, count;  // k_radix_part<k> (or _ms<k>) over RDescs [first, first + count)
-    bool ms;
+    int k, first, count;  // k_radix_part<k> over RDescs [first, first + count)
   };
   struct RadixWave {
     std::vector<RadixLaunch> parts;
@@ -358,8 +357,6 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
                                                         c->hist_smem));
   if (per_sm < 1) return fail(CS_ERR_CUDA, "k_hist does not fit on an SM with %d B smem", c->hist_smem);
   for (RadixPartFn f : kRadixPart)
-    if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
-  for (RadixPartFn f : kRadixPartMS)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_query_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1156,6 +1153,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_nibble = env_int("CS_NIBBLE", 1) != 0;
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const bool knob_radix = env_int("CS_RADIX", 1) != 0;
+  // narrow-counter SMEM class (8 / 16-bit counters with exact wrap repair) for tables of up to
+  // 4x the 32-bit SMEM capacity
+  const bool knob_narrow = env_int("CS_NARROW", 1) != 0;
+  const int64_t knob_narrow_seg = (int64_t)env_int("CS_NARROW_SEG_ROWS", 1 << 24);
   // bitmap class (K7): -1 auto (cost model), 0 never, 1 whenever a query is eligible
   const int knob_bitmap = env_int("CS_BITMAP", -1);
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
@@ -1261,6 +1262,23 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           d.rlog = rh;
         }
       }
+    } else if (knob_narrow && db->nib && k >= 2 && k <= CS_MAXK && c <= 4 * (int64_t)smem_words) {
+      // narrow-counter SMEM class (cs_kernels.cuh hist_smem_narrow): 16-bit counters up to 2x,
+      // 8-bit up to 4x the 32-bit capacity; reads the 4-bit columns
+      d.kind = 0;
+      d.pack = 1;
+      d.rlog = 0;
+      d.mode = 2;
+      d.narrow = c <= 2 * (int64_t)smem_words ? 16 : 8;
+      d.nib = 1;
+      d.base = db->nib;
+      uint32_t r8[8];
+      for (int v = 0; v < 8; ++v) r8[v] = v < k ? (uint32_t)db->arity[vars[b + v]] : 1u;
+      for (int p2 = 0; p2 < 4; ++p2) d.rpair[p2] = r8[2 * p2];
+      d.R0 = r8[0] * r8[1];
+      d.R2 = r8[4] * r8[5];
+      d.P01 = r8[0] * r8[1] * r8[2] * r8[3];
+      for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
     } else if (knob_radix && db->nib && k >= 2 && c <= ((int64_t)1 << 24) &&
                !(knob_slice && c / db->arity[vars[e - 1]] <= smem_words &&
                  slice_passes(c, db->arity[vars[e - 1]]) <= knob_slice_passes)) {
@@ -1294,7 +1312,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
         if (x.half) ct = (ct + 1) / 2;
         return round_up((ct << x.rlog) * 4, 128);
       };
-      if (k <= 4 && knob_stages && !d.scells) {
+      if (k <= 4 && knob_stages && !d.scells && !d.narrow) {
         // shrink packing first if it is what keeps the ring from fitting 3 stages
         while (d.pack > 1 && table_bytes(d) + 3 * per_stage > smem_bytes) {
           d.pack = d.pack == 4 ? 2 : 1;
@@ -1430,7 +1448,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.nseg = 1;
       continue;
     }
-    int64_t nseg = std::max<int64_t>(1, (m + seg_max - 1) / seg_max);
+    const int64_t smax = d.narrow ? std::max(seg_max, knob_narrow_seg) : seg_max;
+    int64_t nseg = std::max<int64_t>(1, (m + smax - 1) / smax);
     const int64_t want = (target_items + nq - 1) / std::max(nq, 1);
     nseg = std::max(nseg, std::min<int64_t>(want, (m + seg_min - 1) / seg_min));
     int64_t L = round_up((m + nseg - 1) / nseg, 256);
@@ -1439,6 +1458,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     if (d.kind == 1) {
       p->score_list.push_back(q);
       p->needs_global = p->needs_zero = true;
+    } else if (d.narrow) {
+      p->needs_global = p->needs_zero = true;  // always merged with global atomics (wrap repairs)
     } else if (d.scells) {
       p->score_list.push_back(q);
       p->needs_global = true;
@@ -1562,13 +1583,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
     for (int q = 0; q < nq; ++q)
       if (p->hq[q].kind == 4) rq.push_back(q);
     if (!rq.empty()) {
-      const bool knob_ms = env_int("CS_RADIX_MS", 1) != 0;
-      auto is_ms = [&](int q) {
-        return knob_ms && (((int64_t)p->hq[q].cells + (1LL << RX_GROUP_BITS) - 1) >> RX_GROUP_BITS) <= RX_MS_MAXG;
-      };
-      std::stable_sort(rq.begin(), rq.end(), [&](int a, int b) {
-        return p->hq[a].k != p->hq[b].k ? p->hq[a].k < p->hq[b].k : (int)is_ms(a) < (int)is_ms(b);
-      });
+      std::stable_sort(rq.begin(), rq.end(), [&](int a, int b) { return p->hq[a].k < p->hq[b].k; });
       const int64_t nchunks = (m + RX_CH - 1) / RX_CH;
       p->rx_nchunks = (int)nchunks;
       const size_t buf_b = (size_t)round_up(nchunks * RX_CH * 2, 256);
@@ -1597,10 +1612,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           r.q = q;
           r.base = d.base;
           const int64_t C = d.cells;
-          const bool ms = is_ms(q);
           int bb = 10;  // >= 32 buckets where possible (SMEM bucket counters contend less)
           while (bb < RX_GROUP_BITS && (C >> (bb + 1)) >= 32) ++bb;
-          if (ms) bb = RX_GROUP_BITS;  // multisplit: one bucket per count group
           r.bb = bb;
           r.nb = (int)((C + (1LL << bb) - 1) >> bb);
           {
@@ -1619,8 +1632,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           r.wlog = wl;
           const int ri = (int)p->rdesc.size();
           p->rdesc.push_back(r);
-          if (wave.parts.empty() || wave.parts.back().k != d.k || wave.parts.back().ms != ms)
-            wave.parts.push_back({d.k, ri, 0, ms});
+          if (wave.parts.empty() || wave.parts.back().k != d.k) wave.parts.push_back({d.k, ri, 0});
           wave.parts.back().count++;
           const int ngrp = (int)((C + (1LL << RX_GROUP_BITS) - 1) >> RX_GROUP_BITS);
           for (int g = 0; g < ngrp; ++g)
@@ -2087,8 +2099,8 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
         const int total = L.count * p->rx_nchunks;
         if (total == 0) continue;
         const int grid = std::min(total, 4 * ctx->num_sms);
-        (L.ms ? kRadixPartMS : kRadixPart)[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(
-            p->d_rdesc + L.first, L.count, p->rx_nchunks, db->m, (char*)scr);
+        kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(p->d_rdesc + L.first, L.count,
+                                                                         p->rx_nchunks, db->m, (char*)scr);
         ctx->launches++;
         CS_CUDA(cudaGetLastError());
       }

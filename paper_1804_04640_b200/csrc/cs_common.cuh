@@ -41,6 +41,11 @@ struct __align__(16) QDesc {
   int32_t nib;                  // 1: columns read from the 4-bit (nibble) copy, 32 rows / 16 B
   int32_t half;                 // 1: 16-bit counters, two cells per word (hist_smem_half)
   uint32_t scells;              // slice class: cells per slice (C / arity of the last digit)
+  int32_t narrow;               // narrow-counter class: counter bits (8 / 16), 0 otherwise
+  // joint index from 4-bit digits d0..d7 in SIMD lanes (narrow class, as cs_radix.cuh RDesc):
+  //   b_p = d_2p + rpair[p] d_2p+1, lo = b0 + R0 b1, hi = b2 + R2 b3, idx = lo + P01 hi
+  uint32_t rpair[4];
+  uint32_t R0, R2, P01;
 };
 
 // One unit of work: rows [r0, r1) of query q.

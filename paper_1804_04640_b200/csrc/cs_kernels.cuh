@@ -607,6 +607,99 @@ __device__ __forceinline__ void hist_smem_packed(const QDesc& q, int64_t r0, int
   }
 }
 
+// SMEM class with narrow counters (QDesc.narrow = BITS = 8 or 16): 32 / BITS cells per 32-bit
+// word, so tables of up to 4x (8-bit) or 2x (16-bit) the 32-bit capacity -- 225K / 112K cells in
+// 220 KB -- are counted in SMEM instead of by the partition class.  A counter that wraps is
+// repaired exactly, without a race: the atomic's old word determines every lane its carry
+// touched (the counted lane wraps to 0 and each wrapped neighbour carries on), and the
+// difference between the true change (+1 on the counted lane) and the stored change of each
+// touched lane goes to the query's global table with one global atomic (modular uint32
+// arithmetic; the epilogue adds the SMEM counters on top).  A wrap costs a few global atomics
+// per 2^BITS increments of one cell.  4-bit columns only (arities <= 16).
+template <int BITS>
+__device__ __noinline__ void narrow_fix(uint32_t old, uint32_t lane, uint32_t cell0, uint32_t C, uint32_t* gtab) {
+  constexpr uint32_t PER = 32 / BITS, MASK = (1u << BITS) - 1u;
+  const uint32_t nw = old + (1u << (lane * BITS));
+  for (uint32_t j = lane; j < PER; ++j) {
+    const int oj = (int)((old >> (j * BITS)) & MASK), nj = (int)((nw >> (j * BITS)) & MASK);
+    const int corr = (j == lane ? 1 : 0) - (nj - oj);
+    if (corr && cell0 + j < C) atomicAdd(gtab + cell0 + j, (uint32_t)corr);
+  }
+}
+
+template <int BITS>
+__device__ __forceinline__ void bump_narrow(uint32_t* sh, uint32_t c, uint32_t C, uint32_t* gtab) {
+  constexpr uint32_t PER = 32 / BITS, MASK = (1u << BITS) - 1u;
+  const uint32_t w = c / PER, lane = c % PER;
+  const uint32_t old = atomicAdd(&sh[w], 1u << (lane * BITS));
+  if (((old >> (lane * BITS)) & MASK) == MASK) narrow_fix<BITS>(old, lane, w * PER, C, gtab);
+}
+
+// joint indices of the 4 rows held by byte lanes of one 4-bit-layout word view (h = 0: low
+// nibbles, h = 1: high nibbles) -- the SIMD-lane scheme of cs_radix.cuh radix_rows
+template <int K>
+__device__ __forceinline__ void nib_joint4(const uint32_t (&x)[K][4], int j, int h, const uint32_t (&rp)[4],
+                                           uint32_t R0, uint32_t R2, uint32_t P01, uint32_t (&idx)[4]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v)
+    w[v] = v < K ? (h ? (x[v < K ? v : 0][j] >> 4) & 0x0f0f0f0fu : x[v < K ? v : 0][j] & 0x0f0f0f0fu) : 0u;
+  uint32_t b[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) b[p] = 2 * p + 1 < K ? w[2 * p] + w[2 * p + 1] * rp[p] : w[2 * p];
+  uint32_t lo01 = __byte_perm(b[0], 0u, 0x4140), lo23 = __byte_perm(b[0], 0u, 0x4342);
+  if (K > 2) {
+    lo01 += __byte_perm(b[1], 0u, 0x4140) * R0;
+    lo23 += __byte_perm(b[1], 0u, 0x4342) * R0;
+  }
+  if (K > 4) {
+    uint32_t hi01 = __byte_perm(b[2], 0u, 0x4140), hi23 = __byte_perm(b[2], 0u, 0x4342);
+    if (K > 6) {
+      hi01 += __byte_perm(b[3], 0u, 0x4140) * R2;
+      hi23 += __byte_perm(b[3], 0u, 0x4342) * R2;
+    }
+    idx[0] = (lo01 & 0xffffu) + P01 * (hi01 & 0xffffu);
+    idx[1] = (lo01 >> 16) + P01 * (hi01 >> 16);
+    idx[2] = (lo23 & 0xffffu) + P01 * (hi23 & 0xffffu);
+    idx[3] = (lo23 >> 16) + P01 * (hi23 >> 16);
+  } else {
+    idx[0] = lo01 & 0xffffu;
+    idx[1] = lo01 >> 16;
+    idx[2] = lo23 & 0xffffu;
+    idx[3] = lo23 >> 16;
+  }
+}
+
+template <int K, int BITS>
+__device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
+                                                 uint32_t* gtab) {
+  const uint8_t* rowp = q.base + (r0 >> 1);
+  uint32_t co[K], rp[4];
+#pragma unroll
+  for (int v = 0; v < K; ++v) co[v] = q.coff[v];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) rp[p] = q.rpair[p];
+  const uint32_t R0 = q.R0, R2 = q.R2, P01 = q.P01, C = q.cells;
+  const int64_t nrows = r1 - r0;
+  const int64_t nvec = (nrows + 31) >> 5;
+  for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+    uint32_t x[K][4];
+    load_vec16<K>(x, rowp + (vi << 4), co);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t idx[4];
+        nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bump_narrow<BITS>(sh, idx[t], C, gtab);
+      }
+    }
+  }
+  const int64_t pad = (nvec << 5) - nrows;  // padding rows (zero nibbles) counted into cell 0
+  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x)) atomicSub(gtab, (uint32_t)pad);
+}
+
 // Other classes: scalar 32-bit index per row.
 //   SMEM=true : SMEM tables too large for 16-bit byte offsets (C*R*4 > 65536);
 //   SMEM=false: RED.ADD into the global table (tables too large for SMEM).
@@ -709,7 +802,8 @@ __device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0,
 // An SMEM item finishes with the fused epilogue: a single-segment query writes its table and
 // scores straight from SMEM; a multi-segment query adds its partial table into global memory
 // and the last segment to arrive (done counter) scores the merged table.
-enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4, P_SLICE = 5 };
+enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4, P_SLICE = 5, P_NARROW8 = 6,
+              P_NARROW16 = 7 };
 constexpr int CS_HIST_THREADS = 1024;
 
 template <int K, int PATH, int NIB>
@@ -741,7 +835,9 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     const uint32_t C = PATH == P_SLICE ? q.scells * (uint32_t)wi.nsl : q.cells;
     uint32_t ct = C;  // cells of the SMEM table (C^pack for packed tuples)
     for (int i = 1; i < pack; ++i) ct *= C;
-    const uint32_t nw = (PATH == P_HALF ? (C + 1u) >> 1 : ct) << rl;
+    constexpr bool NARROW = PATH == P_NARROW8 || PATH == P_NARROW16;
+    constexpr uint32_t NPER = PATH == P_NARROW8 ? 4u : 2u;  // narrow cells per word
+    const uint32_t nw = NARROW ? (C + NPER - 1u) / NPER : (PATH == P_HALF ? (C + 1u) >> 1 : ct) << rl;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
     if (threadIdx.x < 64) s_marg[threadIdx.x] = 0u;
     __syncthreads();
@@ -751,11 +847,16 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     else if (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_SLICE)
       hist_smem_slice<(K >= 2 ? K : 2), NIB>(q, wi.r0, wi.r1, sh, (uint32_t)wi.slice, (uint32_t)wi.nsl);
+    else if (PATH == P_NARROW8) hist_smem_narrow<K, 8>(q, wi.r0, wi.r1, sh, tables + q.table_off);
+    else if (PATH == P_NARROW16) hist_smem_narrow<K, 16>(q, wi.r0, wi.r1, sh, tables + q.table_off);
     else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {
       uint32_t s = 0;
-      if (PATH == P_HALF) {
+      if (NARROW) {
+        constexpr uint32_t B = 32u / NPER;
+        s = (sh[c / NPER] >> ((c % NPER) * B)) & ((1u << B) - 1u);
+      } else if (PATH == P_HALF) {
         const uint32_t p = c >> 1, sh16 = (c & 1u) << 4;
         for (uint32_t r = 0; r < R; ++r) s += (sh[(p << rl) | ((r + p) & (R - 1u))] >> sh16) & 0xffffu;
       } else {
@@ -801,7 +902,7 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
       }
       continue;
     }
-    if (q.nseg == 1) {
+    if (q.nseg == 1 && !NARROW) {  // narrow tables always merge: wrap repairs are already there
       if (tables) {
         uint32_t* t = tables + q.table_off;
         for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) t[c] = cell(c);

@@ -247,190 +247,6 @@ __global__ void __launch_bounds__(RX_THREADS, 4)
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// k_radix_part_ms<K>: the same chunk partition for tables of at most RX_MS_MAXG 32K-cell groups
-// (C <= 31 x 32K cells: ~95% of cfg5's partition-class queries), with the buckets = the count
-// groups (bb = 15) and every per-row SMEM atomic replaced by warp-level multisplit: for each
-// row slot the 32 lanes' group ids are compared with ceil(log2(G + 1)) ballots, which gives
-// each lane the mask of lanes in its group; one leader lane per group bumps the group counter
-// (first pass) or reserves the group's stage slots (second pass) for all of them, and the
-// members write their local index at leader base + rank.  Per 32 rows: 2 conflict-free ATOMS
-// with <= G active lanes instead of 64 random-bank ones (162M of 250M
-// wavefronts were bank-conflict replays).
-constexpr int RX_MS_MAXG = 31;  // groups (+ 1 dummy for rows past m) fit one warp's lanes
-
-__device__ __forceinline__ uint32_t ms_peers(uint32_t g, int nbits) {
-  uint32_t eq = 0xffffffffu;
-  for (int b = 0; b < nbits; ++b) {
-    const uint32_t bit = (g >> b) & 1u;
-    const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-    eq &= bit ? bal : ~bal;
-  }
-  return eq;
-}
-
-// joint indices of one thread's 32-row nibble vector into sidx (rows past m get `dummy`), and
-// the per-group counts via multisplit
-template <int K, bool FULL>
-__device__ __forceinline__ void radix_rows_ms(const uint32_t (&x)[K][4], const uint32_t (&rp)[4], uint32_t R0,
-                                              uint32_t R2, uint32_t P01, uint32_t dummy, int nbits,
-                                              int64_t nvalid, uint32_t* sidx, uint32_t* cnt) {
-  const int tid = threadIdx.x, lane = tid & 31;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint32_t w[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v)
-        w[v] = v < K ? (h ? (x[v < K ? v : 0][j] >> 4) & 0x0f0f0f0fu : x[v < K ? v : 0][j] & 0x0f0f0f0fu) : 0u;
-      uint32_t b[4];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) b[p] = 2 * p + 1 < K ? w[2 * p] + w[2 * p + 1] * rp[p] : w[2 * p];
-      uint32_t lo01 = __byte_perm(b[0], 0u, 0x4140), lo23 = __byte_perm(b[0], 0u, 0x4342);
-      if (K > 2) {
-        lo01 += __byte_perm(b[1], 0u, 0x4140) * R0;
-        lo23 += __byte_perm(b[1], 0u, 0x4342) * R0;
-      }
-      uint32_t idx[4];
-      if (K > 4) {
-        uint32_t hi01 = __byte_perm(b[2], 0u, 0x4140), hi23 = __byte_perm(b[2], 0u, 0x4342);
-        if (K > 6) {
-          hi01 += __byte_perm(b[3], 0u, 0x4140) * R2;
-          hi23 += __byte_perm(b[3], 0u, 0x4342) * R2;
-        }
-        idx[0] = (lo01 & 0xffffu) + P01 * (hi01 & 0xffffu);
-        idx[1] = (lo01 >> 16) + P01 * (hi01 >> 16);
-        idx[2] = (lo23 & 0xffffu) + P01 * (hi23 & 0xffffu);
-        idx[3] = (lo23 >> 16) + P01 * (hi23 >> 16);
-      } else {
-        idx[0] = lo01 & 0xffffu;
-        idx[1] = lo01 >> 16;
-        idx[2] = lo23 & 0xffffu;
-        idx[3] = lo23 >> 16;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int rr = 8 * j + 2 * q + h;
-        const uint32_t i = (FULL || rr < nvalid) ? idx[q] : dummy;
-        sidx[rr * RX_THREADS + tid] = i;
-        const uint32_t g = i >> RX_GROUP_BITS;
-        const uint32_t eq = ms_peers(g, nbits);
-        if (lane == __ffs(eq) - 1) atomicAdd(&cnt[g], (uint32_t)__popc(eq));
-      }
-    }
-  }
-}
-
-template <int K>
-__global__ void __launch_bounds__(RX_THREADS, 4)
-    k_radix_part_ms(const RDesc* __restrict__ rd, int nrq, int nchunks, int64_t m, char* __restrict__ scratch) {
-  extern __shared__ uint32_t rsm[];
-  uint32_t* sidx = rsm;                                        // [32][RX_THREADS] joint indices
-  uint16_t* stage = reinterpret_cast<uint16_t*>(rsm + RX_CH);  // RX_CH local indices, group-sorted
-  uint32_t* cnt = rsm + RX_CH + RX_CH / 2;                     // group counts, then cursors
-  const int tid = threadIdx.x, lane = tid & 31;
-  if ((int64_t)blockIdx.x >= (int64_t)nrq * nchunks) return;
-  int rq = (int)(blockIdx.x / nchunks), c = (int)(blockIdx.x % nchunks);
-  int cur = -1;
-  bool have = false;
-  uint32_t x[K][4];
-  auto load_vectors = [&](uint32_t (&xx)[K][4], const uint8_t* b, const uint32_t (&co)[K], int64_t r0) {
-    if (r0 < m) {
-      const uint8_t* p = b + (r0 >> 1);
-#pragma unroll
-      for (int v = 0; v < K; ++v) {
-        const uint4 t = ldg_stream16(p + ((uint64_t)co[v] << 8));
-        xx[v][0] = t.x;
-        xx[v][1] = t.y;
-        xx[v][2] = t.z;
-        xx[v][3] = t.w;
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < K; ++v) xx[v][0] = xx[v][1] = xx[v][2] = xx[v][3] = 0u;
-    }
-  };
-  const uint8_t* base = nullptr;
-  uint32_t coff[K], rp[4], R0 = 0, R2 = 0, P01 = 0;
-  int nb = 0, nbits = 1;
-  char* buf = nullptr;
-  int32_t* choff = nullptr;
-  for (; rq < nrq;) {
-    if (rq != cur) {
-      const RDesc& r = rd[rq];
-      base = r.base;
-#pragma unroll
-      for (int v = 0; v < K; ++v) coff[v] = r.coff[v];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) rp[p] = r.rpair[p];
-      R0 = r.R0;
-      R2 = r.R2;
-      P01 = r.P01;
-      nb = r.nb;  // groups
-      nbits = 32 - __clz(nb);  // bits of the ids 0..nb (nb = the dummy group)
-      buf = scratch + r.buf_off;
-      choff = reinterpret_cast<int32_t*>(scratch + r.choff_off);
-      cur = rq;
-    }
-    if (tid <= nb) cnt[tid] = 0u;
-    const int64_t row0 = (int64_t)c * RX_CH + (int64_t)tid * 32;
-    if (!have) load_vectors(x, base, coff, row0);
-    const int64_t nvalid = m - row0;
-    const uint32_t dummy = (uint32_t)nb << RX_GROUP_BITS;
-    __syncthreads();  // cnt zeroed
-    // a chunk is full unless it holds row m-1: every warp then takes the same branch
-    if ((int64_t)(c + 1) * RX_CH <= m)
-      radix_rows_ms<K, true>(x, rp, R0, R2, P01, dummy, nbits, nvalid, sidx, cnt);
-    else
-      radix_rows_ms<K, false>(x, rp, R0, R2, P01, dummy, nbits, nvalid, sidx, cnt);
-    int c2 = c + gridDim.x, rq2 = rq;
-    while (c2 >= nchunks) {
-      c2 -= nchunks;
-      ++rq2;
-    }
-    have = rq2 == rq;
-    if (have) load_vectors(x, base, coff, (int64_t)c2 * RX_CH + (int64_t)tid * 32);
-    __syncthreads();
-    // exclusive scan of the <= 32 group counts by warp 0 (the dummy group last)
-    if (tid < 32) {
-      const uint32_t v = tid <= nb ? cnt[tid] : 0u;
-      uint32_t incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (tid <= nb) {
-        cnt[tid] = incl - v;
-        choff[(int64_t)c * (nb + 1) + tid] = (int32_t)(incl - v);  // [nb] = rows staged
-      }
-    }
-    __syncthreads();
-    const uint32_t nstaged = cnt[nb];
-    // scatter: one reservation per (row slot, group) by the group's leader lane
-#pragma unroll 4
-    for (int rr = 0; rr < 32; ++rr) {
-      const uint32_t i = sidx[rr * RX_THREADS + tid];
-      const uint32_t g = i >> RX_GROUP_BITS;
-      const uint32_t eq = ms_peers(g, nbits);
-      const int leader = __ffs(eq) - 1;
-      uint32_t pos = 0;
-      if (lane == leader) pos = atomicAdd(&cnt[g], (uint32_t)__popc(eq));
-      pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(eq & ((1u << lane) - 1u));
-      if (g < (uint32_t)nb) stage[pos] = (uint16_t)(i & ((1u << RX_GROUP_BITS) - 1u));
-    }
-    __syncthreads();
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(buf) + (int64_t)c * RX_CH);
-    const uint4* src = reinterpret_cast<const uint4*>(stage);
-    const uint32_t nv = (nstaged + 7u) >> 3;
-    for (uint32_t i = tid; i < nv; i += RX_THREADS) dst[i] = src[i];
-    __syncthreads();
-    c = c2;
-    rq = rq2;
-  }
-}
-
 __device__ __forceinline__ uint4 ldg_nc16(const void* p) {
   uint4 r;
   asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
