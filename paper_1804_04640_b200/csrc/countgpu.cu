@@ -1157,6 +1157,9 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   // 4x the 32-bit SMEM capacity
   const bool knob_narrow = env_int("CS_NARROW", 1) != 0;
   const int64_t knob_narrow_seg = (int64_t)env_int("CS_NARROW_SEG_ROWS", 1 << 24);
+  // more than 4x the capacity: several passes (cell ranges) over each L2-resident row segment
+  const int64_t knob_narrow_passes = std::max(1, env_int("CS_NARROW_MAX_PASSES", 1));
+  const int64_t knob_narrow_pass_seg = (int64_t)env_int("CS_NARROW_PASS_SEG_ROWS", 1 << 22);
   // bitmap class (K7): -1 auto (cost model), 0 never, 1 whenever a query is eligible
   const int knob_bitmap = env_int("CS_BITMAP", -1);
   const int64_t knob_seg_max = (int64_t)env_int("CS_SEG_MAX_ROWS", 1 << 22);
@@ -1262,7 +1265,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
           d.rlog = rh;
         }
       }
-    } else if (knob_narrow && db->nib && k >= 2 && k <= CS_MAXK && c <= 4 * (int64_t)smem_words) {
+    } else if (knob_narrow && db->nib && k >= 2 && k <= CS_MAXK &&
+               c <= 4 * (int64_t)smem_words * knob_narrow_passes) {
       // narrow-counter SMEM class (cs_kernels.cuh hist_smem_narrow): 16-bit counters up to 2x,
       // 8-bit up to 4x the 32-bit capacity; reads the 4-bit columns
       d.kind = 0;
@@ -1270,6 +1274,8 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.rlog = 0;
       d.mode = 2;
       d.narrow = c <= 2 * (int64_t)smem_words ? 16 : 8;
+      d.npass = (int32_t)((c + 4 * (int64_t)smem_words - 1) / (4 * (int64_t)smem_words));
+      d.pcells = (uint32_t)round_up((c + d.npass - 1) / d.npass, 4);
       d.nib = 1;
       d.base = db->nib;
       uint32_t r8[8];
@@ -1448,7 +1454,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.nseg = 1;
       continue;
     }
-    const int64_t smax = d.narrow ? std::max(seg_max, knob_narrow_seg) : seg_max;
+    const int64_t smax = d.narrow ? (d.npass > 1 ? knob_narrow_pass_seg : std::max(seg_max, knob_narrow_seg)) : seg_max;
     int64_t nseg = std::max<int64_t>(1, (m + smax - 1) / smax);
     const int64_t want = (target_items + nq - 1) / std::max(nq, 1);
     nseg = std::max(nseg, std::min<int64_t>(want, (m + seg_min - 1) / seg_min));
@@ -1468,7 +1474,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       p->needs_global = p->needs_zero = true;
     }
     // slice class: a CTA owns as many consecutive last-digit values as its SMEM holds
-    const int rlast = d.scells ? (int)(d.cells / d.scells) : 1;
+    const int rlast = d.scells ? (int)(d.cells / d.scells) : (d.narrow ? d.npass : 1);
     const int spc = d.scells ? std::max(1, (int)(smem_words / ((int64_t)d.scells << d.rlog))) : 1;
     for (int64_t s = 0; s < nseg; ++s) {
       for (int sl = 0; sl < rlast; sl += spc) {

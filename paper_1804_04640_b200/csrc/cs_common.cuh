@@ -46,6 +46,8 @@ struct __align__(16) QDesc {
   //   b_p = d_2p + rpair[p] d_2p+1, lo = b0 + R0 b1, hi = b2 + R2 b3, idx = lo + P01 hi
   uint32_t rpair[4];
   uint32_t R0, R2, P01;
+  int32_t npass;                // narrow class: passes over each row segment (cell ranges)
+  uint32_t pcells;              // narrow class: cells per pass (multiple of 4)
 };
 
 // One unit of work: rows [r0, r1) of query q.

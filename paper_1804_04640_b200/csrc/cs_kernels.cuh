@@ -670,16 +670,18 @@ __device__ __forceinline__ void nib_joint4(const uint32_t (&x)[K][4], int j, int
   }
 }
 
+// One pass counts the cells [lo, lo + C) (several passes over an L2-resident row segment when
+// the table exceeds one SM even with 8-bit counters); rows outside the range are skipped.
 template <int K, int BITS>
 __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
-                                                 uint32_t* gtab) {
+                                                 uint32_t* gtab, uint32_t lo, uint32_t C) {
   const uint8_t* rowp = q.base + (r0 >> 1);
   uint32_t co[K], rp[4];
 #pragma unroll
   for (int v = 0; v < K; ++v) co[v] = q.coff[v];
 #pragma unroll
   for (int p = 0; p < 4; ++p) rp[p] = q.rpair[p];
-  const uint32_t R0 = q.R0, R2 = q.R2, P01 = q.P01, C = q.cells;
+  const uint32_t R0 = q.R0, R2 = q.R2, P01 = q.P01;
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + 31) >> 5;
   for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
@@ -692,12 +694,16 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
         uint32_t idx[4];
         nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bump_narrow<BITS>(sh, idx[t], C, gtab);
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t rel = idx[t] - lo;
+          if (rel < C) bump_narrow<BITS>(sh, rel, C, gtab);
+        }
       }
     }
   }
   const int64_t pad = (nvec << 5) - nrows;  // padding rows (zero nibbles) counted into cell 0
-  if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x)) atomicSub(gtab, (uint32_t)pad);
+  if (lo == 0 && pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
+    atomicSub(gtab, (uint32_t)pad);
 }
 
 // Other classes: scalar 32-bit index per row.
@@ -832,10 +838,13 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     const QDesc& q = s_q;
     const int rl = q.rlog;
     const uint32_t R = 1u << rl;
-    const uint32_t C = PATH == P_SLICE ? q.scells * (uint32_t)wi.nsl : q.cells;
+    constexpr bool NARROW = PATH == P_NARROW8 || PATH == P_NARROW16;
+    // narrow class: this item's pass covers cells [plo, plo + C) of the query's table
+    const uint32_t plo = NARROW ? (uint32_t)wi.slice * q.pcells : 0u;
+    const uint32_t C = PATH == P_SLICE ? q.scells * (uint32_t)wi.nsl
+                       : (NARROW && q.npass > 1 ? min(q.pcells, q.cells - plo) : q.cells);
     uint32_t ct = C;  // cells of the SMEM table (C^pack for packed tuples)
     for (int i = 1; i < pack; ++i) ct *= C;
-    constexpr bool NARROW = PATH == P_NARROW8 || PATH == P_NARROW16;
     constexpr uint32_t NPER = PATH == P_NARROW8 ? 4u : 2u;  // narrow cells per word
     const uint32_t nw = NARROW ? (C + NPER - 1u) / NPER : (PATH == P_HALF ? (C + 1u) >> 1 : ct) << rl;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
@@ -847,8 +856,8 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     else if (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
     else if (PATH == P_SLICE)
       hist_smem_slice<(K >= 2 ? K : 2), NIB>(q, wi.r0, wi.r1, sh, (uint32_t)wi.slice, (uint32_t)wi.nsl);
-    else if (PATH == P_NARROW8) hist_smem_narrow<K, 8>(q, wi.r0, wi.r1, sh, tables + q.table_off);
-    else if (PATH == P_NARROW16) hist_smem_narrow<K, 16>(q, wi.r0, wi.r1, sh, tables + q.table_off);
+    else if (PATH == P_NARROW8) hist_smem_narrow<K, 8>(q, wi.r0, wi.r1, sh, tables + q.table_off + plo, plo, C);
+    else if (PATH == P_NARROW16) hist_smem_narrow<K, 16>(q, wi.r0, wi.r1, sh, tables + q.table_off + plo, plo, C);
     else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {
@@ -918,17 +927,18 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
       uint32_t* t = tables + q.table_off;
       for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
         const uint32_t v = cell(c);
-        if (v) atomicAdd(t + c, v);
+        if (v) atomicAdd(t + plo + c, v);
       }
       if (want_score) {
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s_last = (atomicAdd(done + wi.q, 1u) == (uint32_t)(q.nseg - 1));
+        const uint32_t parts = (uint32_t)q.nseg * (NARROW ? (uint32_t)q.npass : 1u);
+        if (threadIdx.x == 0) s_last = (atomicAdd(done + wi.q, 1u) == parts - 1u);
         __syncthreads();
         if (s_last) {
           __threadfence();
           auto gcell = [&](uint32_t c) -> uint32_t { return __ldcg(t + c); };
-          score_table(gcell, C, q.r_target, m_total, flags, wi.q, ll_out, mi_out, nnz_out, ss);
+          score_table(gcell, NARROW ? q.cells : C, q.r_target, m_total, flags, wi.q, ll_out, mi_out, nnz_out, ss);
         }
       }
     }

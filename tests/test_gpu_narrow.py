@@ -106,3 +106,22 @@ def test_narrow_off_matches_partition(ctx, monkeypatch):
     gdb2 = GpuDatabase.from_columns(ctx, data2, ar2)
     qs2 = [(0, 1, 2, 3, 4, 5), (5, 4, 3, 2, 1, 0)]  # 98,304 cells: 16-bit narrow
     _check(gdb2, data2, ar2, qs2)
+
+
+@pytest.mark.parametrize("m", [70_001, 4_500_000])
+def test_narrow_multipass(ctx, monkeypatch, capfd, m):
+    """Tables above 4x the SMEM capacity in several cell-range passes (CS_NARROW_MAX_PASSES):
+    uniform cells plus a hot cell whose 8-bit counter wraps in every pass's range."""
+    monkeypatch.setenv("CS_NARROW_MAX_PASSES", "8")
+    monkeypatch.setenv("CS_TRACE", "1")
+    rng = np.random.default_rng(m)
+    ar = [16, 16, 16, 16, 6, 5]
+    data = np.vstack([rng.integers(0, a, m) for a in ar]).astype(np.uint8)
+    hot = rng.random(m) < 0.3
+    data[:, hot] = np.array([3, 1, 4, 1, 5, 2], dtype=np.uint8)[:, None]
+    gdb = GpuDatabase.from_columns(ctx, data, ar)
+    qs = [(0, 1, 2, 3, 4), (4, 3, 2, 1, 0), (0, 1, 2, 3, 5), (5, 0, 1, 2, 3), (1, 2, 3, 4, 5)]
+    _check(gdb, data, ar, qs)  # 393,216 / 327,680 / 122,880 cells: 2 passes, 2 passes, 1
+    assert _classes(capfd)["partition"] == 0
+    monkeypatch.setenv("CS_NARROW_PASS_SEG_ROWS", "65536")
+    _check(gdb, data, ar, qs)
