@@ -685,35 +685,27 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + 31) >> 5;
   constexpr uint32_t PER = 32 / BITS, MASK = (1u << BITS) - 1u;
-  uint32_t x[K][4], xn[K][4];
-  if ((int64_t)threadIdx.x < nvec) load_vec16<K>(x, rowp + ((int64_t)threadIdx.x << 4), co);
   for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
-    // next vector in flight while this one is counted
-    const int64_t vn = vi + blockDim.x;
-    if (vn < nvec) load_vec16<K>(xn, rowp + (vn << 4), co);
+    uint32_t x[K][4];
+    load_vec16<K>(x, rowp + (vi << 4), co);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // the 8 rows of word view j: all atomics issued before any wrap test reads a result
-      uint32_t rel[8], old[8];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        uint32_t idx[4];
+        // the 4 rows of one word view: all atomics issued before any wrap test reads a result
+        uint32_t idx[4], old[4];
         nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) rel[4 * h + t] = idx[t] - lo;
+        for (int t = 0; t < 4; ++t) {
+          idx[t] -= lo;
+          old[t] = idx[t] < C ? atomicAdd(&sh[idx[t] / PER], 1u << ((idx[t] % PER) * BITS)) : 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (idx[t] < C && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK)
+            narrow_fix<BITS>(old[t], idx[t] % PER, idx[t] / PER * PER, C, gtab);
       }
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        old[t] = rel[t] < C ? atomicAdd(&sh[rel[t] / PER], 1u << ((rel[t] % PER) * BITS)) : 0u;
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        if (rel[t] < C && ((old[t] >> ((rel[t] % PER) * BITS)) & MASK) == MASK)
-          narrow_fix<BITS>(old[t], rel[t] % PER, rel[t] / PER * PER, C, gtab);
     }
-#pragma unroll
-    for (int v = 0; v < K; ++v)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) x[v][e] = xn[v][e];
   }
   const int64_t pad = (nvec << 5) - nrows;  // padding rows (zero nibbles) counted into cell 0
   if (lo == 0 && pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
