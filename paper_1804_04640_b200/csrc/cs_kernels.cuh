@@ -18,6 +18,8 @@
 //   K5 k_compact       non-zero cell stream (n_ijk, n_ij, cell) for record aggregators.
 //      k_generate      counter-based column generator (device twin of oracle/gen_twin.py).
 #pragma once
+#include <type_traits>
+
 #include "cs_common.cuh"
 
 namespace cs {
@@ -685,28 +687,41 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + 31) >> 5;
   constexpr uint32_t PER = 32 / BITS, MASK = (1u << BITS) - 1u;
-  for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
-    uint32_t x[K][4];
-    load_vec16<K>(x, rowp + (vi << 4), co);
+  // RANGED: a pass over part of the table (rows outside [lo, lo + C) skipped); the single-pass
+  // loop has no range test (every joint index is a cell)
+  auto run = [&](auto ranged) {
+    constexpr bool RANGED = decltype(ranged)::value;
+    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+      uint32_t x[K][4];
+      load_vec16<K>(x, rowp + (vi << 4), co);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 4; ++j) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        // the 4 rows of one word view: all atomics issued before any wrap test reads a result
-        uint32_t idx[4], old[4];
-        nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
+        for (int h = 0; h < 2; ++h) {
+          // the 4 rows of one word view: all atomics issued before any wrap test reads a result
+          uint32_t idx[4], old[4];
+          nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          idx[t] -= lo;
-          old[t] = idx[t] < C ? atomicAdd(&sh[idx[t] / PER], 1u << ((idx[t] % PER) * BITS)) : 0u;
+          for (int t = 0; t < 4; ++t) {
+            if (RANGED) idx[t] -= lo;
+            old[t] = (!RANGED || idx[t] < C) ? atomicAdd(&sh[idx[t] / PER], 1u << ((idx[t] % PER) * BITS)) : 0u;
+          }
+          bool wrap = false;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            wrap |= (!RANGED || idx[t] < C) && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK;
+          if (wrap) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if ((!RANGED || idx[t] < C) && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK)
+                narrow_fix<BITS>(old[t], idx[t] % PER, idx[t] / PER * PER, C, gtab);
+          }
         }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (idx[t] < C && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK)
-            narrow_fix<BITS>(old[t], idx[t] % PER, idx[t] / PER * PER, C, gtab);
       }
     }
-  }
+  };
+  if (lo == 0 && C == q.cells) run(std::false_type{});
+  else run(std::true_type{});
   const int64_t pad = (nvec << 5) - nrows;  // padding rows (zero nibbles) counted into cell 0
   if (lo == 0 && pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(gtab, (uint32_t)pad);
