@@ -321,22 +321,42 @@ class QueryRunner:
         # one device table buffer: a step executes every plan (the whole stream)
         chunk = int(os.environ.get("CS_BENCH_CHUNK", "2000"))
         self.chunks = []
-        if not self.sharded and len(self.queries) > chunk:
-            for c0 in range(0, len(self.queries), chunk):
-                c1 = min(len(self.queries), c0 + chunk)
+        self.shard_runs = []
+        self.merge = None
+        cuts = list(range(0, len(self.queries), chunk)) + [len(self.queries)]
+        if self.sharded:
+            # instance sharding: consecutive CHUNK-query runners sharing one table buffer.
+            # CS_BENCH_MERGE=reduce_scatter (default): partial tables reduce-scattered to their
+            # owners, owners score, scores all-gathered; =allreduce: all-reduce, everyone scores
+            from paper_1804_04640_b200 import parallel as PAR
+
+            self.merge = os.environ.get("CS_BENCH_MERGE", "reduce_scatter")
+            ar = w.arities
+            cells = [[int(np.prod([int(ar[v]) for v in q], dtype=np.int64)) for q in self.queries[a:b]]
+                     for a, b in zip(cuts[:-1], cuts[1:])]
+            if self.merge == "allreduce":
+                tb = torch.empty(max(sum(c) for c in cells), dtype=torch.int32, device="cuda")
+                for a, b in zip(cuts[:-1], cuts[1:]):
+                    self.shard_runs.append((a, b, PAR.InstanceShardedPlan(self.gdb, self.queries[a:b], tables=tb)))
+            else:
+                S = max(max(sum(c[i] for i in o) for o in PAR.owner_split(c, world)) for c in cells)
+                buf = torch.zeros((world + 1) * (-(-S // 64) * 64), dtype=torch.int32, device="cuda")
+                for a, b in zip(cuts[:-1], cuts[1:]):
+                    self.shard_runs.append((a, b, PAR.ReduceScatterInstanceSharded(
+                        self.gdb, self.queries[a:b], world, rank, buf=buf)))
+            self.plan = self.shard_runs[0][2].plans[0] if self.merge != "allreduce" else self.shard_runs[0][2].plan
+            self.kernel_is_step = True
+        elif len(self.queries) > chunk:
+            for c0, c1 in zip(cuts[:-1], cuts[1:]):
                 self.chunks.append((c0, c1, QueryPlan(self.gdb, self.queries[c0:c1], flags)))
             self.plan = max((p for _, _, p in self.chunks), key=lambda p: p.total_cells)
             self.kernel_is_step = True  # the library's events bracket one plan; time the step
         else:
             self.plan = QueryPlan(self.gdb, self.queries, flags)
         self.units = len(self.queries)
-        if self.sharded:
-            from paper_1804_04640_b200.parallel import PipelinedInstanceSharded
-
-            self.pipe = PipelinedInstanceSharded(self.gdb, self.queries, nbatch=4)
         dev = "cuda"
         self.tables = (torch.empty(max(self.plan.total_cells, 1), dtype=torch.int32, device=dev)
-                       if (self.want_tables or self.sharded or self.chunks) else None)
+                       if (self.want_tables or self.chunks) and not self.sharded else None)
         self.ll = torch.empty(self.units, dtype=torch.float64, device=dev) if self.want_ll else None
         self.mi = torch.empty(self.units, dtype=torch.float64, device=dev) if self.want_mi else None
         self.algo_bytes = float(sum(len(q) for q in self.queries)) * self.rows
@@ -350,14 +370,14 @@ class QueryRunner:
         self.d2h = int((self.plan.total_cells * 4 if self.want_tables else 0)
                        + self.units * 8 * (int(self.want_ll) + int(self.want_mi)))
         self.scaling = "strong" if self.sharded else "weak"
-        self.parallelism = (f"instance-shard x{world} + NCCL all-reduce" if self.sharded
-                            else f"query-shard x{world}")
+        self.parallelism = ((f"instance-shard x{world} + NCCL " +
+                             ("all-reduce" if self.merge == "allreduce" else "reduce-scatter + owner scoring"))
+                            if self.sharded else f"query-shard x{world}")
 
     def step(self):
         if self.sharded:
-            # four query slices: slice b's NCCL all-reduce (uint32 sum == int32 sum bitwise)
-            # overlaps slice b+1's scan; each slice is scored after its merge
-            self.pipe.run(loglik=self.ll, mi=self.mi)
+            for a, b, run in self.shard_runs:
+                run.run(loglik=self.ll[a:b], mi=self.mi[a:b])
         elif self.chunks:
             for c0, c1, p in self.chunks:
                 p.execute(tables=self.tables, loglik=None if self.ll is None else self.ll[c0:c1],

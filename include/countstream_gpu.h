@@ -201,6 +201,32 @@ int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint
 int cs_family_scores(cs_ctx* ctx, int64_t nfam, const double* nlogn, int64_t nsub, const int32_t* s_idx,
                      const int32_t* p_idx, const double* penalty, double m_ln_m, double* ll, double* mdl);
 
+/* ---- multi-GPU: instance sharding (survey 8(e)) ---------------------------------------------
+ * Contract.  Rank g of N holds rows [r0, r0 + m_g) of the database (cs_db_create on that row
+ * range, or cs_db_generate with row_offset = r0: the generator keys every state on the GLOBAL
+ * row id, so shards reproduce the unsharded columns) and declares the global row count with
+ * cs_db_set_total_rows(db, m).  Every rank plans the same queries with CS_PARTIAL: tables are
+ * the shard's counts and no score is computed.  Counts are additive over disjoint row ranges, so
+ * summing the partial tables over ranks (cs_reduce_tables, or any all-reduce / reduce-scatter of
+ * uint32 / int32 words) gives the unsharded tables bit-exactly; cs_plan_score on merged tables
+ * scores with the global m (MI's 1/m, MDL's ln m).  With REDUCE_SCATTER each rank receives the
+ * merged tables of the queries it owns (a contiguous, equal-size slice of the table buffer:
+ * one plan per owner, each writing its own slice) and scores only those.
+ * NCCL (libnccl.so.2) is opened at run time; CS_ERR_UNSUPPORTED when it cannot be. */
+#define CS_REDUCE_ALLREDUCE 0
+#define CS_REDUCE_SCATTER 1
+/* id: 128 bytes (ncclUniqueId), created on one rank and sent to the others by the caller */
+int cs_comm_unique_id(void* id);
+int cs_comm_init(cs_ctx* ctx, const void* id, int32_t rank, int32_t nranks);
+int cs_comm_destroy(cs_ctx* ctx);
+/* Sum uint32 tables over the ranks on the context stream (asynchronous).  tables, out: device.
+ * ALLREDUCE: cells words, in place when out is NULL.  REDUCE_SCATTER: cells = nranks * S;
+ * rank r receives the merged words [r S, (r + 1) S) in out (S words). */
+int cs_reduce_tables(cs_ctx* ctx, uint32_t* tables, int64_t cells, int32_t op, uint32_t* out);
+/* Every rank's `bytes` of send, concatenated in rank order into recv (device; the owners'
+ * fp64 scores after a REDUCE_SCATTER merge).  Asynchronous on the context stream. */
+int cs_comm_all_gather(cs_ctx* ctx, const void* send, int64_t bytes, void* recv);
+
 /* ---- point counts / itemset supports (reference bitmap.py:131-136, radix.py:181-193) - */
 /* counts[q] = #records with vars[j] == states[j] for every j in query q.  Uses bitmap
  * planes when every (var, state) has one (AND + popcount), else a byte scan. */

@@ -34,6 +34,9 @@ CS_WANT_NNZ = 0x8
 CS_PARTIAL = 0x10
 CS_NLOGN = 0x20
 
+CS_REDUCE_ALLREDUCE = 0
+CS_REDUCE_SCATTER = 1
+
 # (name, restype, argtypes) for every symbol declared in include/countstream_gpu.h
 _P = c_void_p
 SIGNATURES = [
@@ -69,6 +72,11 @@ SIGNATURES = [
     ("cs_family_scores", c_int, [_P, c_int64, _P, c_int64, _P, _P, _P, c_double, _P, _P]),
     ("cs_query_batch", c_int, [_P, c_int32, _P, _P, c_uint32, _P, _P, _P, _P]),
     ("cs_query_one", c_int, [_P, c_int32, _P, c_uint32, _P, _P, _P, _P]),
+    ("cs_comm_unique_id", c_int, [_P]),
+    ("cs_comm_init", c_int, [_P, _P, c_int32, c_int32]),
+    ("cs_comm_destroy", c_int, [_P]),
+    ("cs_reduce_tables", c_int, [_P, _P, c_int64, c_int32, _P]),
+    ("cs_comm_all_gather", c_int, [_P, _P, c_int64, _P]),
     ("cs_count_points", c_int, [_P, c_int32, _P, _P, _P, _P]),
     ("cs_itemset_supports", c_int, [_P, c_int32, _P, _P, _P]),
 ]

@@ -27,6 +27,7 @@
 #include "cs_itemsets_sel.cuh"
 #include "cs_bitmapq.cuh"
 #include "cs_one.cuh"
+#include "cs_comm.cuh"
 
 using namespace cs;
 
@@ -166,6 +167,9 @@ struct cs_ctx {
   char* mbox = nullptr;
   char* mbox_dev = nullptr;
   uint32_t one_seq = 0;
+  // instance-shard merge (cs_comm_init): NCCL communicator of this context's device
+  ncclComm_t comm = nullptr;
+  int comm_rank = 0, comm_size = 1;
 
   int scratch_get(int slot, size_t bytes, void** out) {
     auto& s = scratch[slot + 1000 * bank];
@@ -399,6 +403,7 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned1) cudaFreeHost(ctx->pinned1);
   if (ctx->mbox) cudaFreeHost(ctx->mbox);
+  if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -2435,6 +2440,92 @@ extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t 
   CS_TRY(put(mi, o + 1, 8));
   CS_TRY(put(nnz, o + 2, 8));
   if (table && !table_dev) memcpy(table, ctx->mbox + 64, (size_t)C * 4);
+  return CS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// instance-shard merge (NCCL; cs_comm.cuh)
+
+#define CS_NCCL(call)                                                                         \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(CS_ERR_CUDA, "%s failed: %s", #call, nccl_api().GetErrorString(r_));        \
+  } while (0)
+
+extern "C" int cs_comm_unique_id(void* id) {
+  if (!id) return fail(CS_ERR_INVALID, "cs_comm_unique_id: NULL id");
+  NcclApi& a = nccl_api();
+  if (!a.ok) return fail(CS_ERR_UNSUPPORTED, "%s", a.err.c_str());
+  ncclUniqueId u;
+  CS_NCCL(a.GetUniqueId(&u));
+  memcpy(id, &u, sizeof u);
+  return CS_OK;
+}
+
+extern "C" int cs_comm_init(cs_ctx* ctx, const void* id, int32_t rank, int32_t nranks) {
+  CtxLock lk_(ctx);
+  if (!ctx || !id) return fail(CS_ERR_INVALID, "cs_comm_init: NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CS_ERR_INVALID, "cs_comm_init: rank %d of %d", rank, nranks);
+  NcclApi& a = nccl_api();
+  if (!a.ok) return fail(CS_ERR_UNSUPPORTED, "%s", a.err.c_str());
+  CS_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->comm) {
+    a.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof u);
+  CS_NCCL(a.CommInitRank(&ctx->comm, nranks, u, rank));
+  ctx->comm_rank = rank;
+  ctx->comm_size = nranks;
+  return CS_OK;
+}
+
+extern "C" int cs_comm_destroy(cs_ctx* ctx) {
+  CtxLock lk_(ctx);
+  if (!ctx) return fail(CS_ERR_INVALID, "cs_comm_destroy: NULL ctx");
+  if (ctx->comm) {
+    CS_CUDA(cudaSetDevice(ctx->device));
+    CS_NCCL(nccl_api().CommDestroy(ctx->comm));
+    ctx->comm = nullptr;
+  }
+  ctx->comm_rank = 0;
+  ctx->comm_size = 1;
+  return CS_OK;
+}
+
+extern "C" int cs_reduce_tables(cs_ctx* ctx, uint32_t* tables, int64_t cells, int32_t op, uint32_t* out) {
+  CtxLock lk_(ctx);
+  if (!ctx || !tables) return fail(CS_ERR_INVALID, "cs_reduce_tables: NULL argument");
+  if (!ctx->comm) return fail(CS_ERR_INVALID, "cs_reduce_tables: call cs_comm_init first");
+  if (cells < 0) return fail(CS_ERR_INVALID, "cs_reduce_tables: cells < 0");
+  if (!is_device_ptr(tables) || (out && !is_device_ptr(out)))
+    return fail(CS_ERR_INVALID, "cs_reduce_tables: tables must be device memory");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  NcclApi& a = nccl_api();
+  // uint32 counts summed as uint32 (m < 2^32 keeps every merged count exact)
+  if (op == CS_REDUCE_ALLREDUCE) {
+    CS_NCCL(a.AllReduce(tables, out ? out : tables, (size_t)cells, ncclUint32, ncclSum, ctx->comm, ctx->stream));
+  } else if (op == CS_REDUCE_SCATTER) {
+    if (cells % ctx->comm_size) return fail(CS_ERR_INVALID, "cs_reduce_tables: %lld cells not a multiple of %d ranks",
+                                            (long long)cells, ctx->comm_size);
+    if (!out) return fail(CS_ERR_INVALID, "cs_reduce_tables: REDUCE_SCATTER needs an output buffer");
+    CS_NCCL(a.ReduceScatter(tables, out, (size_t)(cells / ctx->comm_size), ncclUint32, ncclSum, ctx->comm, ctx->stream));
+  } else {
+    return fail(CS_ERR_INVALID, "cs_reduce_tables: bad op %d", op);
+  }
+  return CS_OK;
+}
+
+extern "C" int cs_comm_all_gather(cs_ctx* ctx, const void* send, int64_t bytes, void* recv) {
+  CtxLock lk_(ctx);
+  if (!ctx || !send || !recv) return fail(CS_ERR_INVALID, "cs_comm_all_gather: NULL argument");
+  if (!ctx->comm) return fail(CS_ERR_INVALID, "cs_comm_all_gather: call cs_comm_init first");
+  if (!is_device_ptr(send) || !is_device_ptr(recv))
+    return fail(CS_ERR_INVALID, "cs_comm_all_gather: buffers must be device memory");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  CS_NCCL(nccl_api().AllGather(send, recv, (size_t)bytes, ncclUint8, ctx->comm, ctx->stream));
   return CS_OK;
 }
 

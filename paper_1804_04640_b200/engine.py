@@ -101,6 +101,30 @@ class GpuContext:
         check(lib.cs_ctx_itemset_class(self._h, byref(v)))
         return {0: "none", 1: "bitgemm", 2: "tensor", 3: "selector"}[int(v.value)]
 
+    # -- instance-shard merge through the C ABI (NCCL opened by the library) ------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """A fresh 128-byte NCCL unique id (create on one rank, send to the others)."""
+        buf = ctypes.create_string_buffer(128)
+        check(lib.cs_comm_unique_id(buf))
+        return buf.raw
+
+    def comm_init(self, uid: bytes, rank: int, nranks: int) -> None:
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(lib.cs_comm_init(self._h, buf, int(rank), int(nranks)))
+
+    def comm_destroy(self) -> None:
+        check(lib.cs_comm_destroy(self._h))
+
+    def reduce_tables(self, tables, op: int = 0, out=None, cells: int | None = None) -> None:
+        """Sum device uint32/int32 tables over the communicator (cs_reduce_tables)."""
+        n = int(tables.numel()) if cells is None else int(cells)
+        check(lib.cs_reduce_tables(self._h, ptr(tables), n, int(op), ptr(out)))
+
+    def all_gather(self, send, recv) -> None:
+        """recv (device) = every rank's send (device) concatenated in rank order."""
+        check(lib.cs_comm_all_gather(self._h, ptr(send), int(send.numel() * send.element_size()), ptr(recv)))
+
     def info(self) -> dict:
         a, b, c = c_int32(), c_int32(), c_int32()
         check(lib.cs_ctx_info(self._h, byref(a), byref(b), byref(c)))

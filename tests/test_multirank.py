@@ -58,6 +58,23 @@ def _worker(rank, world, port, q):
         sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(sizes, torch.tensor([len(idx)], dtype=torch.int64))
         ok_cover = int(sum(int(s) for s in sizes)) == len(w.queries)
+        # reduce-scatter ownership (parallel.ReduceScatterInstanceSharded's layout): every rank
+        # lays its partial tables out per owner in a world x S buffer; one reduce-scatter leaves
+        # each owner exactly the merged tables of its queries
+        cells = [int(np.prod([int(w.arities[v]) for v in qq])) for qq in w.queries]
+        owned = parallel.owner_split(cells, world)
+        S = max(sum(cells[i] for i in o) for o in owned)
+        buf = np.zeros(world * S, dtype=np.uint32)
+        for r, o in enumerate(owned):
+            pt, _, _, _ = O.radix_tables(np.ascontiguousarray(u8[:, r0:r0 + nr]), w.arities, [w.queries[i] for i in o])
+            buf[r * S: r * S + len(pt)] = pt
+        out = torch.zeros(S, dtype=torch.int32)
+        dist.reduce_scatter_tensor(out, torch.from_numpy(buf.view(np.int32)))
+        mine_full, _, mine_ll, _ = O.radix_tables(u8, w.arities, [w.queries[i] for i in owned[rank]])
+        ok_rs = bool(np.array_equal(out.numpy().view(np.uint32)[: len(mine_full)], mine_full))
+        ok_rs &= bool((out.numpy()[len(mine_full):] == 0).all())
+        ok_cover &= sorted(i for o in owned for i in o) == list(range(len(w.queries)))
+        ok_tables &= ok_rs
         q.put((rank, ok_tables, ok_gather, ok_cover, nr))
     finally:
         dist.destroy_process_group()
