@@ -160,6 +160,9 @@ def counting_roofline(r, k_ms: float) -> dict:
     input_bytes = r.algo_bytes * bpr
     ks = k_ms / 1e3
     traffic = load_traffic(r.config)
+    if traffic is None and r.config == "cfg5":
+        per_q = load_traffic("cfg5_per_query")
+        traffic = per_q * r.units if per_q else None
     hbm = {"peak": peak_hbm, "peak_source": src_hbm, "logical_bytes": r.algo_bytes,
            "logical_frac": r.algo_bytes / ks / 1e9 / peak_hbm,
            "dram_bytes": traffic, "dram_frac": (traffic / ks / 1e9 / peak_hbm) if traffic else None}
