@@ -162,7 +162,7 @@ def counting_roofline(r, k_ms: float) -> dict:
     traffic = load_traffic(r.config)
     if traffic is None and r.config == "cfg5":
         per_q = load_traffic("cfg5_per_query")
-        traffic = per_q * r.units if per_q else None
+        traffic = per_q * r.units * (r.rows / r.w.m) if per_q else None  # rows: this rank's shard
     hbm = {"peak": peak_hbm, "peak_source": src_hbm, "logical_bytes": r.algo_bytes,
            "logical_frac": r.algo_bytes / ks / 1e9 / peak_hbm,
            "dram_bytes": traffic, "dram_frac": (traffic / ks / 1e9 / peak_hbm) if traffic else None}
