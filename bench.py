@@ -322,7 +322,8 @@ class QueryRunner:
         self.flags = flags
         # long streams (cfg5's 100,000 queries) run as consecutive plans of CHUNK queries sharing
         # one device table buffer: a step executes every plan (the whole stream)
-        chunk = int(os.environ.get("CS_BENCH_CHUNK", "2000"))
+        # (cfg5 only: the other configs' batches are one plan, as the reference-facing call is)
+        chunk = int(os.environ.get("CS_BENCH_CHUNK", "2000")) if args.config == "cfg5" else 1 << 30
         self.chunks = []
         self.shard_runs = []
         self.merge = None
