@@ -193,6 +193,12 @@ int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, const int32_t*
  * cs_query_batch.  Synchronous. */
 int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table, double* loglik,
                  double* mi, int64_t* nnz);
+/* The same query's non-zero cells (the reference's record stream, radix.py:143-156 /
+ * bitmap.py:103-116) in cell order: cell index, N_ijk, N_ij (host int64[cells] each; *nnz =
+ * how many were written).  Only for queries of the single-query class (CS_ERR_UNSUPPORTED
+ * otherwise: use a plan and cs_plan_compact). */
+int cs_query_one_cells(cs_db* db, int32_t k, const int32_t* vars, int64_t* cell_idx, int64_t* n_ijk,
+                       int64_t* n_ij, int64_t* nnz);
 
 /* Batched MDL parent-set scoring (learn_parents, harness.py:296-348; MdlScore,
  * aggregators.py:163-193).  nlogn[nsub]: CS_NLOGN outputs of a plan over the distinct variable

@@ -72,6 +72,7 @@ SIGNATURES = [
     ("cs_family_scores", c_int, [_P, c_int64, _P, c_int64, _P, _P, _P, c_double, _P, _P]),
     ("cs_query_batch", c_int, [_P, c_int32, _P, _P, c_uint32, _P, _P, _P, _P]),
     ("cs_query_one", c_int, [_P, c_int32, _P, c_uint32, _P, _P, _P, _P]),
+    ("cs_query_one_cells", c_int, [_P, c_int32, _P, _P, _P, _P, _P]),
     ("cs_comm_unique_id", c_int, [_P]),
     ("cs_comm_init", c_int, [_P, _P, c_int32, c_int32]),
     ("cs_comm_destroy", c_int, [_P]),

@@ -2364,8 +2364,22 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
 }
 
 // one query, latency class (K8, cs_one.cuh)
+static int query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table, double* loglik,
+                     double* mi, int64_t* nnz, int64_t* cell_idx, int64_t* n_ijk, int64_t* n_ij);
+
 extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table,
                             double* loglik, double* mi, int64_t* nnz) {
+  return query_one(db, k, vars, flags, table, loglik, mi, nnz, nullptr, nullptr, nullptr);
+}
+
+extern "C" int cs_query_one_cells(cs_db* db, int32_t k, const int32_t* vars, int64_t* cell_idx, int64_t* n_ijk,
+                                  int64_t* n_ij, int64_t* nnz) {
+  if (!cell_idx || !n_ijk || !n_ij || !nnz) return fail(CS_ERR_INVALID, "cs_query_one_cells: NULL output");
+  return query_one(db, k, vars, 0, nullptr, nullptr, nullptr, nnz, cell_idx, n_ijk, n_ij);
+}
+
+static int query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t flags, uint32_t* table, double* loglik,
+                     double* mi, int64_t* nnz, int64_t* cell_idx, int64_t* n_ijk, int64_t* n_ij) {
   CtxLock lk_(db ? db->ctx : nullptr);
   if (!db) return fail(CS_ERR_INVALID, "cs_query_one: NULL db");
   if (k < 1) return fail(CS_ERR_INVALID, "query 0 has no target variable");
@@ -2384,13 +2398,17 @@ extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t 
   const bool one = k <= CS_MAXK && C <= ONE_MAX_CELLS && db->m <= max_rows && !(flags & (F_PARTIAL | F_NLOGN)) &&
                    env_int("CS_ONE", 1) != 0;
   if (!one) {  // the batch path (transient plan) answers everything else
+    if (cell_idx)
+      return fail(CS_ERR_UNSUPPORTED, "cs_query_one_cells: query outside the single-query class (use a plan + "
+                                      "cs_plan_compact)");
     const int32_t off[2] = {0, k};
     return cs_query_batch(db, 1, off, vars, flags, table, loglik, mi, nnz);
   }
   cs_ctx* ctx = db->ctx;
   CS_CUDA(cudaSetDevice(ctx->device));
   if (!ctx->mbox) {
-    CS_CUDA(cudaHostAlloc((void**)&ctx->mbox, 64 + (size_t)ONE_MAX_CELLS * 4, cudaHostAllocMapped));
+    CS_CUDA(cudaHostAlloc((void**)&ctx->mbox, 64 + (size_t)ONE_MAX_CELLS * 4 + (size_t)ONE_MAX_CELLS * 24,
+                          cudaHostAllocMapped));
     CS_CUDA(cudaHostGetDevicePointer((void**)&ctx->mbox_dev, ctx->mbox, 0));
   }
   OneQ q;
@@ -2410,6 +2428,7 @@ extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t 
   const bool table_dev = table && is_device_ptr(table);
   q.table = table ? (table_dev ? table : (uint32_t*)(ctx->mbox_dev + 64)) : nullptr;
   q.out = (double*)ctx->mbox_dev;
+  q.cells_out = cell_idx ? (int64_t*)(ctx->mbox_dev + 64 + (size_t)ONE_MAX_CELLS * 4) : nullptr;
   q.done = (volatile uint32_t*)(ctx->mbox_dev + 32);
   q.seq = ++ctx->one_seq;
   volatile uint32_t* done = (volatile uint32_t*)(ctx->mbox + 32);
@@ -2440,6 +2459,13 @@ extern "C" int cs_query_one(cs_db* db, int32_t k, const int32_t* vars, uint32_t 
   CS_TRY(put(mi, o + 1, 8));
   CS_TRY(put(nnz, o + 2, 8));
   if (table && !table_dev) memcpy(table, ctx->mbox + 64, (size_t)C * 4);
+  if (cell_idx) {
+    const int64_t nz = ((const int64_t*)ctx->mbox)[2];
+    const int64_t* src = (const int64_t*)(ctx->mbox + 64 + (size_t)ONE_MAX_CELLS * 4);
+    memcpy(cell_idx, src, sizeof(int64_t) * nz);
+    memcpy(n_ijk, src + C, sizeof(int64_t) * nz);
+    memcpy(n_ij, src + 2 * C, sizeof(int64_t) * nz);
+  }
   return CS_OK;
 }
 

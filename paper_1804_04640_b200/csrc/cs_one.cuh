@@ -28,6 +28,8 @@ struct OneQ {
   int64_t m;
   double m_total;
   uint32_t* table;  // mapped host (or device) dense table, or NULL
+  int64_t* cells_out;  // mapped host: [3][cells] cell index, N_ijk, N_ij of the non-zero cells in
+                       // cell order (the record stream), or NULL; their count goes to out[2]
   double* out;      // [0] LL, [1] MI, [2] nnz (int64 bits)
   volatile uint32_t* done;  // mapped host word: set to `seq` once every result above is visible
   uint32_t seq;
@@ -54,6 +56,48 @@ __global__ void __launch_bounds__(ONE_THREADS, 1) k_query_one(const OneQ q) {
   __syncthreads();
   if (q.table)
     for (uint32_t c = tid; c < q.cells; c += ONE_THREADS) q.table[c] = one_tab[c];
+  if (q.cells_out) {
+    // non-zero cells in cell order: each thread owns a contiguous run of whole configurations
+    // (r_t cells), counts its non-zeros, a block scan places them
+    __shared__ uint32_t s_wsum[ONE_THREADS / 32];
+    const uint32_t J = q.cells / (uint32_t)q.r_t;
+    const uint32_t per = (J + ONE_THREADS - 1) / ONE_THREADS;
+    const uint32_t j0 = min(J, tid * per), j1 = min(J, j0 + per);
+    uint32_t mine = 0;
+    for (uint32_t c = j0 * q.r_t; c < j1 * q.r_t; ++c) mine += one_tab[c] != 0;
+    uint32_t incl = mine;
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+    for (int w = 0; w < ONE_THREADS / 32; ++w) {
+      if (w < warp) pre += s_wsum[w];
+      tot += s_wsum[w];
+    }
+    uint32_t pos = pre + incl - mine;
+    int64_t* oi = q.cells_out;
+    int64_t* on = oi + q.cells;
+    int64_t* oj = on + q.cells;
+    for (uint32_t j = j0; j < j1; ++j) {
+      uint32_t nij = 0;
+      for (int k = 0; k < q.r_t; ++k) nij += one_tab[j * q.r_t + k];
+      for (int k = 0; k < q.r_t; ++k) {
+        const uint32_t c = j * q.r_t + k, x = one_tab[c];
+        if (x) {
+          oi[pos] = c;
+          on[pos] = x;
+          oj[pos] = nij;
+          ++pos;
+        }
+      }
+    }
+    if (tid == 0) reinterpret_cast<int64_t*>(q.out)[2] = tot;
+  }
   if (q.flags & (F_LOGLIK | F_MI | F_NNZ)) {
     auto cell = [&](uint32_t c) { return one_tab[c]; };
     score_table(cell, q.cells, q.r_t, q.m_total, q.flags, 0, q.out, q.out + 1,

@@ -207,9 +207,9 @@ class GpuStrategy(Strategy):
             self.gdb.bitmap_build()
 
     # -- drop-in per-query API ------------------------------------------------------------
-    #: dense tables up to this many cells come back whole and are compacted on the host (one
-    #: engine call); larger ones are compacted on the device (K5) through a plan
-    HOST_COMPACT_CELLS = 1 << 16
+    #: tables up to this many cells (the single-query class, cs_query_one_cells) stream their
+    #: non-zero cells from the one-launch kernel; larger ones are compacted by K5 through a plan
+    ONE_CELLS = 48 * 1024
 
     def query(self, q: QuerySpec, agg) -> None:
         """One query through cs_query_one (K8 latency class: one launch, descriptor as a kernel
@@ -237,32 +237,34 @@ class GpuStrategy(Strategy):
         cells = 1
         for v in vs:
             cells *= int(ar[v])
-        if cells <= min(self.HOST_COMPACT_CELLS, _dense_limit()):
-            tb = self._tls.__dict__.get("tab")
-            if tb is None:
-                buf = np.zeros(self.HOST_COMPACT_CELLS, dtype=np.uint32)
-                vb = np.zeros(64, dtype=np.int32)
-                tb = self._tls.tab = (buf, buf.ctypes.data, vb, vb.ctypes.data)
-            buf, ba, vb, va = tb
-            if len(vs) <= len(vb):
-                vb[:len(vs)] = vs
-                N.check(N.lib.cs_query_one(self.gdb.handle, len(vs), va, N.CS_WANT_TABLES, ba, None, None, None))
-            else:
-                self.gdb.query_one(np.array(vs, dtype=np.int32), N.CS_WANT_TABLES, tables=buf)
-            tab = buf[:cells]
-            r_t = int(ar[vs[0]])
-            nij_all = tab.reshape(-1, r_t).sum(axis=1, dtype=np.int64)
-            cidx = np.flatnonzero(tab)
-            nijk = tab[cidx].astype(np.int64)
-            nij = nij_all[cidx // r_t]
-        else:
+        got = None
+        if cells <= min(self.ONE_CELLS, _dense_limit()) and len(vs) <= 8:
+            # the record stream straight from the single-query kernel (cell order), or
+            # CS_ERR_UNSUPPORTED when the query is outside its class
+            sc = self._tls.__dict__.get("cells")
+            if sc is None:
+                bufs = np.zeros((3, self.ONE_CELLS), dtype=np.int64)
+                nz = np.zeros(1, dtype=np.int64)
+                vb = np.zeros(8, dtype=np.int32)
+                sc = self._tls.cells = (bufs, nz, vb, bufs[0].ctypes.data, bufs[1].ctypes.data,
+                                        bufs[2].ctypes.data, nz.ctypes.data, vb.ctypes.data)
+            bufs, nz, vb, a0, a1, a2, an, va = sc
+            vb[:len(vs)] = vs
+            rc = N.lib.cs_query_one_cells(self.gdb.handle, len(vs), va, a0, a1, a2, an)
+            if rc == N.CS_OK:
+                n = int(nz[0])
+                got = (bufs[0, :n], bufs[1, :n].copy(), bufs[2, :n].copy())
+            elif rc != N.CS_ERR_UNSUPPORTED:
+                N.check(rc)
+        if got is None:
             with self._lock:
                 plan = QueryPlan(self.gdb, [vs], N.CS_WANT_TABLES)
                 nnz = np.zeros(1, dtype=np.int64)
                 plan.execute(nnz=nnz)
                 _, cidx, nijk, nij = plan.compact(None, nnz)
                 plan.close()
-        self._deliver(q, agg, cidx, nijk, nij)
+            got = (cidx, nijk, nij)
+        self._deliver(q, agg, *got)
 
     def _deliver(self, q: QuerySpec, agg, cidx, nijk, nij) -> None:
         if not getattr(agg, "wants_records", False):

@@ -102,3 +102,42 @@ def test_strategy_query_all_aggregators(reference_cases):
         sink = cs.NullSink()
         s.query(qs, sink)
         assert sink.count == len(golden_records(q))
+
+
+def test_query_one_cells_record_stream(ctx):
+    """cs_query_one_cells: the non-zero cells in cell order with N_ij; CS_ERR_UNSUPPORTED for a
+    query outside the single-query class (the strategy then compacts through a plan)."""
+    import ctypes
+
+    from paper_1804_04640_b200 import _native as N
+
+    rng = np.random.default_rng(12)
+    m = 30_000
+    ar = [3, 4, 2, 5, 250, 200]
+    data = np.vstack([rng.integers(0, a, m) for a in ar]).astype(np.uint8)
+    data[1, data[0] == 2] = 0  # structural zeros
+    gdb = GpuDatabase.from_columns(ctx, data, ar)
+    for q in [(0,), (1, 0), (3, 1, 0, 2), (2, 3)]:
+        cells = int(np.prod([ar[v] for v in q]))
+        ci, a, b = (np.zeros(cells, np.int64) for _ in range(3))
+        nz = np.zeros(1, np.int64)
+        v = np.asarray(q, np.int32)
+        N.check(N.lib.cs_query_one_cells(gdb.handle, len(q), v.ctypes.data, ci.ctypes.data, a.ctypes.data,
+                                         b.ctypes.data, nz.ctypes.data))
+        t, _, _, _, _ = O.dense_tables(data, ar, [q])
+        want = np.flatnonzero(t)
+        n = int(nz[0])
+        assert np.array_equal(ci[:n], want)
+        assert np.array_equal(a[:n], t[want])
+        r_t = ar[q[0]]
+        assert np.array_equal(b[:n], t.reshape(-1, r_t).sum(axis=1)[want // r_t])
+    v = np.asarray((4, 5), np.int32)  # 50,000 cells: outside the class
+    big = np.zeros(50_000, np.int64)
+    nz = np.zeros(1, np.int64)
+    rc = N.lib.cs_query_one_cells(gdb.handle, 2, v.ctypes.data, big.ctypes.data, big.ctypes.data,
+                                  big.ctypes.data, nz.ctypes.data)
+    assert rc == N.CS_ERR_UNSUPPORTED
+    s = cs.GpuStrategy(cs.Database(data.astype(np.int32), ar))
+    col = cs.RecordCollector()
+    s.query(cs.QuerySpec(4, (5,)), col)  # through the plan + K5 path
+    assert len(col.result()) == int(np.count_nonzero(O.dense_tables(data, ar, [(4, 5)])[0]))
