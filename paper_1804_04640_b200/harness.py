@@ -272,20 +272,21 @@ class GpuStrategy(Strategy):
             return
         ar = self.db.arities
         r_t = int(ar[q.target])
-        radices = [int(ar[p]) for p in q.parents]
-        order = sorted(range(len(q.parents)), key=lambda t: q.parents[t])
-        ks = (cidx % r_t).tolist()
-        js = (cidx // r_t).tolist()
-        a, b = nijk.tolist(), nij.tolist()
         parents = q.parents
+        js = cidx // r_t
+        # each parent's state of every record, vectorised (cell = k + r_t (s_p0 + r_p0 (s_p1 ...)))
+        states = {}
+        stride = 1
+        for p in parents:
+            r = int(ar[p])
+            states[p] = ((js // stride) % r).tolist()
+            stride *= r
+        ordered = sorted(parents)
+        configs = zip(*[zip(itertools.repeat(p), states[p]) for p in ordered]) if parents else \
+            itertools.repeat((), len(js))
         accept = agg.accept_record
-        for t in range(len(js)):
-            j = js[t]
-            states = []
-            for r in radices:
-                j, s = divmod(j, r)
-                states.append(s)
-            accept(tuple((parents[u], states[u]) for u in order), ks[t], a[t], b[t])
+        for cfg, k, x, n in zip(configs, (cidx % r_t).tolist(), nijk.tolist(), nij.tolist()):
+            accept(cfg, k, x, n)
 
     def count(self, a: Assignment) -> int:
         a.validate(self.db)
