@@ -23,6 +23,7 @@
 #include "cs_kernels.cuh"
 #include "cs_itemsets.cuh"
 #include "cs_radix.cuh"
+#include "cs_spill.cuh"
 #include "cs_ingest.cuh"
 #include "cs_itemsets_sel.cuh"
 #include "cs_bitmapq.cuh"
@@ -108,6 +109,10 @@ static const HistFn kHist[CS_MAXK][8][3] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(
 
 // K1r partition kernels per digit count (k >= 2)
 using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
+using SpillHistFn = void (*)(const SDesc*, const SItem*, int, int*, uint32_t*, char*);
+static const SpillHistFn kSpillHist[CS_MAXK] = {nullptr,         k_spill_hist<2>, k_spill_hist<3>,
+                                                k_spill_hist<4>, k_spill_hist<5>, k_spill_hist<6>,
+                                                k_spill_hist<7>, k_spill_hist<8>};
 static const RadixPartFn kRadixPart[CS_MAXK] = {nullptr,         k_radix_part<2>, k_radix_part<3>,
                                                 k_radix_part<4>, k_radix_part<5>, k_radix_part<6>,
                                                 k_radix_part<7>, k_radix_part<8>};
@@ -170,6 +175,12 @@ struct cs_ctx {
   // instance-shard merge (cs_comm_init): NCCL communicator of this context's device
   ncclComm_t comm = nullptr;
   int comm_rank = 0, comm_size = 1;
+  // side streams of the histogram phase (cs_plan_execute): the per-variant persistent kernels of
+  // one plan are spread over the context stream and these, forked and joined with events, so a
+  // kernel's tail (SMs idle while its last items finish) is filled by the next kernel's CTAs
+  static constexpr int NSIDE = 3;
+  cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[NSIDE] = {nullptr, nullptr, nullptr};
 
   int scratch_get(int slot, size_t bytes, void** out) {
     auto& s = scratch[slot + 1000 * bank];
@@ -260,6 +271,19 @@ struct cs_plan {
   RDesc* d_rdesc = nullptr;
   RItem* d_ritems = nullptr;
   int* d_rhead = nullptr;  // one work-queue head per wave
+  // kind 6 (spill class, cs_spill.cuh): waves sharing context scratch slot 24
+  struct SpillWave {
+    std::vector<RadixLaunch> parts;  // k_spill_hist<k> over SItems [first, first + count)
+    int item0 = 0, nitems = 0;       // k_spill_count items
+  };
+  std::vector<SDesc> sdesc;
+  std::vector<SpillWave> swaves;
+  size_t sp_scratch = 0;
+  int sp_heads = 0;  // work-queue heads: one per k_spill_hist launch and one per wave
+  SDesc* d_sdesc = nullptr;
+  SItem* d_sitems = nullptr;
+  CItem* d_citems = nullptr;
+  int* d_shead = nullptr;
   struct Group {
     int key, first, count;
   };
@@ -363,6 +387,10 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
   for (RadixPartFn f : kRadixPart)
     if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, RX_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_radix_count, cudaFuncAttributeMaxDynamicSharedMemorySize, RC_SMEM));
+  for (SpillHistFn f : kSpillHist)
+    if (f) CS_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+  CS_CUDA(cudaFuncSetAttribute((const void*)k_spill_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               SP_COUNT_SMEM));
   CS_CUDA(cudaFuncSetAttribute((const void*)k_query_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(ONE_MAX_CELLS * 4)));
   for (int k = 1; k <= BQ_MAXK; ++k)
@@ -389,6 +417,11 @@ extern "C" int cs_ctx_create(int32_t device, cs_ctx** out) {
                                200 * 1024));
   CS_CUDA(cudaEventCreate(&c->ev0));
   CS_CUDA(cudaEventCreate(&c->ev1));
+  CS_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+  for (int i = 0; i < cs_ctx::NSIDE; ++i) {
+    CS_CUDA(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking));
+    CS_CUDA(cudaEventCreateWithFlags(&c->join_ev[i], cudaEventDisableTiming));
+  }
   c->hist_ctas = per_sm * c->num_sms;
   *out = c;
   return CS_OK;
@@ -408,6 +441,14 @@ extern "C" int cs_ctx_destroy(cs_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  for (int i = 0; i < cs_ctx::NSIDE; ++i) {
+    if (ctx->side[i]) {
+      cudaStreamSynchronize(ctx->side[i]);
+      cudaStreamDestroy(ctx->side[i]);
+    }
+    if (ctx->join_ev[i]) cudaEventDestroy(ctx->join_ev[i]);
+  }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return CS_OK;
@@ -1158,6 +1199,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   const bool knob_nibble = env_int("CS_NIBBLE", 1) != 0;
   const bool knob_slice = env_int("CS_SLICE", 1) != 0;
   const bool knob_radix = env_int("CS_RADIX", 1) != 0;
+  // spill class (cs_spill.cuh): the first hist_smem cells counted in SMEM, the other rows' indices
+  // moved once and counted per 192K-cell group (<= CS_SPILL_GROUPS groups)
+  const bool knob_spill = env_int("CS_SPILL", 1) != 0;
+  const int64_t spill_t1 = (int64_t)(ctx->hist_smem / 4) * 4;
+  const int64_t spill_max =
+      spill_t1 + (int64_t)SP_GROUP_CELLS * std::max(1, std::min(SP_MAXG, env_int("CS_SPILL_GROUPS", 2)));
   // narrow-counter SMEM class (8 / 16-bit counters with exact wrap repair) for tables of up to
   // 4x the 32-bit SMEM capacity
   const bool knob_narrow = env_int("CS_NARROW", 1) != 0;
@@ -1289,6 +1336,12 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.R0 = r8[0] * r8[1];
       d.R2 = r8[4] * r8[5];
       d.P01 = r8[0] * r8[1] * r8[2] * r8[3];
+      for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
+    } else if (knob_spill && db->nib && k >= 2 && k <= CS_MAXK && c > spill_t1 && c <= spill_max) {
+      d.kind = 6;
+      d.mode = 2;
+      d.nib = 1;
+      d.base = db->nib;
       for (int i = 0; i < k; ++i) d.coff[i] = (uint32_t)((int64_t)vars[b + i] * (db->ldn / 256));
     } else if (knob_radix && db->nib && k >= 2 && c <= ((int64_t)1 << 24) &&
                !(knob_slice && c / db->arity[vars[e - 1]] <= smem_words &&
@@ -1446,7 +1499,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       d.nseg = 1;
       continue;
     }
-    if (d.kind == 4 || d.kind == 5) {
+    if (d.kind == 4 || d.kind == 5 || d.kind == 6) {
       p->score_list.push_back(q);
       p->needs_global = p->needs_zero = true;
       d.nseg = 1;
@@ -1655,6 +1708,108 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       }
     }
   }
+  // spill class (kind 6): waves of queries whose spill regions share one context scratch; per
+  // wave one k_spill_hist launch per digit count over (query, row segment) items, then
+  // k_spill_count over (query, range group, row segment) items
+  std::vector<SItem> sitems;
+  std::vector<CItem> citems;
+  if (nkind[6]) {
+    std::vector<int> sq;
+    for (int q = 0; q < nq; ++q)
+      if (p->hq[q].kind == 6) sq.push_back(q);
+    std::stable_sort(sq.begin(), sq.end(), [&](int a, int b) { return p->hq[a].k < p->hq[b].k; });
+    const double slack = std::max(0, env_int("CS_SPILL_SLACK", 125)) / 100.0;
+    const int64_t seg_rows = std::max<int64_t>(1 << 16, env_int("CS_SPILL_SEG_ROWS", 1 << 23));
+    const int64_t n0 = std::max<int64_t>(1, (m + seg_rows - 1) / seg_rows);
+    size_t budget = (size_t)env_int("CS_SPILL_MB", 4096) << 20;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 2);
+    else cudaGetLastError();
+    // scratch of one query split into nseg segments: one stream of cap entries per (segment, warp)
+    struct Lay {
+      int64_t L, nseg, cap, regions;
+      size_t reg_b, cnt_b;
+    };
+    auto layout = [&](int64_t C, int64_t nseg) {
+      Lay y;
+      y.L = round_up((m + nseg - 1) / nseg, 256);
+      y.nseg = (m + y.L - 1) / y.L;
+      const int64_t nvec = (y.L + 31) / 32;
+      const int64_t rows_warp = (nvec + SP_THREADS - 1) / SP_THREADS * 1024;  // 32 lanes x 32 rows per iteration
+      // the uniform expectation times the slack, plus the 1024 entries one vector may append
+      const double expect = (double)rows_warp * (double)(C - spill_t1) / (double)C;
+      y.cap = slack > 0 ? round_up(std::min<int64_t>(rows_warp, (int64_t)std::ceil(expect * slack)) + 1024, 4) : 0;
+      y.regions = y.nseg * SP_WARPS;
+      y.reg_b = (size_t)round_up(y.regions * y.cap * 4, 256);
+      y.cnt_b = (size_t)round_up(y.regions * 4, 256);
+      return y;
+    };
+    size_t i0 = 0;
+    while (i0 < sq.size()) {
+      // greedy wave under the budget, sized with the finest segmentation it may get
+      size_t i1 = i0, bytes = 0;
+      while (i1 < sq.size()) {
+        const Lay y = layout(p->cells[sq[i1]], 2 * n0);
+        if (i1 > i0 && bytes + y.reg_b + y.cnt_b > budget) break;
+        bytes += y.reg_b + y.cnt_b;
+        ++i1;
+      }
+      // segments per query: n0 .. 2 n0, whichever fills the persistent grid's rounds best
+      const int64_t W = (int64_t)(i1 - i0);
+      int64_t nseg = n0;
+      double best = -1.0;
+      for (int64_t c = n0; c <= 2 * n0; ++c) {
+        const int64_t it = W * c, rounds = (it + ctx->num_sms - 1) / ctx->num_sms;
+        const double eff = (double)it / (double)(rounds * ctx->num_sms);
+        if (eff > best + 1e-9) {
+          best = eff;
+          nseg = c;
+        }
+      }
+      cs_plan::SpillWave wave;
+      wave.item0 = (int)citems.size();
+      size_t off = 0;
+      for (size_t i = i0; i < i1; ++i) {
+        const int q = sq[i];
+        const QDesc& d = p->hq[q];
+        const Lay y = layout(p->cells[q], nseg);
+        SDesc r;
+        memset(&r, 0, sizeof r);
+        r.base = d.base;
+        r.table_off = d.table_off;
+        r.reg_off = (int64_t)off;
+        r.cnt_off = (int64_t)(off + y.reg_b);
+        off += y.reg_b + y.cnt_b;
+        uint32_t r8[8];
+        for (int v = 0; v < 8; ++v) r8[v] = v < d.k ? (uint32_t)db->arity[vars[var_off[q] + v]] : 1u;
+        for (int p2 = 0; p2 < 4; ++p2) r.rpair[p2] = r8[2 * p2];
+        r.R0 = r8[0] * r8[1];
+        r.R2 = r8[4] * r8[5];
+        r.P01 = r8[0] * r8[1] * r8[2] * r8[3];
+        for (int v = 0; v < d.k; ++v) r.coff[v] = d.coff[v];
+        r.cells = d.cells;
+        r.t1 = (uint32_t)spill_t1;
+        r.cap = (uint32_t)y.cap;
+        r.ng = (int32_t)((p->cells[q] - spill_t1 + SP_GROUP_CELLS - 1) / SP_GROUP_CELLS);
+        r.nseg = (int32_t)y.nseg;
+        r.q = q;
+        const int si = (int)p->sdesc.size();
+        p->sdesc.push_back(r);
+        if (wave.parts.empty() || wave.parts.back().k != d.k) wave.parts.push_back({d.k, (int)sitems.size(), 0});
+        for (int64_t g = 0; g < y.nseg; ++g) {
+          sitems.push_back(SItem{si, (int32_t)g, g * y.L, std::min(m, (g + 1) * y.L)});
+          wave.parts.back().count++;
+        }
+        for (int grp = 0; grp < r.ng; ++grp)
+          for (int64_t g = 0; g < y.nseg; ++g) citems.push_back(CItem{si, grp, (int32_t)g, 0});
+      }
+      p->sp_scratch = std::max(p->sp_scratch, off);
+      p->sp_heads += (int)wave.parts.size() + 1;
+      wave.nitems = (int)citems.size() - wave.item0;
+      p->swaves.push_back(wave);
+      i0 = i1;
+    }
+  }
   // bitmap class (kind 5): (query, tile range) items grouped by digit count
   std::vector<BItem> bitems;
   if (!p->bdesc.empty()) {
@@ -1677,9 +1832,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   }
   const double tr2 = trace ? now_ms() : 0.0;
   if (trace)
-    fprintf(stderr, "plan_build: classes smem=%lld global=%lld generic=%lld hash=%lld partition=%lld bitmap=%lld\n",
+    fprintf(stderr,
+            "plan_build: classes smem=%lld global=%lld generic=%lld hash=%lld partition=%lld bitmap=%lld spill=%lld\n",
             (long long)nkind[0], (long long)nkind[1], (long long)nkind[2], (long long)nkind[3], (long long)nkind[4],
-            (long long)nkind[5]);
+            (long long)nkind[5], (long long)nkind[6]);
   if (trace)
     fprintf(stderr, "plan_build: setup %.3f ms, classify %.3f ms (parallel part %.3f), items %.3f ms, order %.3f ms\n",
             trs - trc, tr0 - trs, trp - trs, tr1 - tr0,
@@ -1705,7 +1861,11 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
                orh = place(sizeof(int) * std::max<size_t>(p->waves.size(), 1)),
                obd = place(sizeof(BDesc) * std::max<size_t>(p->bdesc.size(), 1)),
                obi = place(sizeof(BItem) * std::max<size_t>(bitems.size(), 1)),
-               obh = place(sizeof(int) * BQ_MAXK);
+               obh = place(sizeof(int) * BQ_MAXK),
+               osd = place(sizeof(SDesc) * std::max<size_t>(p->sdesc.size(), 1)),
+               osi = place(sizeof(SItem) * std::max<size_t>(sitems.size(), 1)),
+               oci = place(sizeof(CItem) * std::max<size_t>(citems.size(), 1)),
+               osh = place(sizeof(int) * std::max(p->sp_heads, 1));
   char* dblob = nullptr;
   p->transient = transient;
   if (transient) {
@@ -1745,11 +1905,16 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   memcpy(hs + ori, ritems.data(), sizeof(RItem) * ritems.size());
   memcpy(hs + obd, p->bdesc.data(), sizeof(BDesc) * p->bdesc.size());
   memcpy(hs + obi, bitems.data(), sizeof(BItem) * bitems.size());
+  memcpy(hs + osd, p->sdesc.data(), sizeof(SDesc) * p->sdesc.size());
+  memcpy(hs + osi, sitems.data(), sizeof(SItem) * sitems.size());
+  memcpy(hs + oci, citems.data(), sizeof(CItem) * citems.size());
   CS_CUDA(cudaMemcpyAsync(dblob, hs, oh, cudaMemcpyHostToDevice, ctx->stream));
   if (!p->rdesc.empty())
     CS_CUDA(cudaMemcpyAsync(dblob + ord, hs + ord, orh - ord, cudaMemcpyHostToDevice, ctx->stream));
   if (!p->bdesc.empty())
     CS_CUDA(cudaMemcpyAsync(dblob + obd, hs + obd, obh - obd, cudaMemcpyHostToDevice, ctx->stream));
+  if (!p->sdesc.empty())
+    CS_CUDA(cudaMemcpyAsync(dblob + osd, hs + osd, osh - osd, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->pipe) {
     auto& ev = ctx->stage_ev[ctx->bank];
     if (!ev) CS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1770,6 +1935,10 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
   p->d_bdesc = (BDesc*)(dblob + obd);
   p->d_bitems = (BItem*)(dblob + obi);
   p->d_bhead = (int*)(dblob + obh);
+  p->d_sdesc = (SDesc*)(dblob + osd);
+  p->d_sitems = (SItem*)(dblob + osi);
+  p->d_citems = (CItem*)(dblob + oci);
+  p->d_shead = (int*)(dblob + osh);
   if (trace) fprintf(stderr, "plan_build: upload %.3f ms\n", now_ms() - tr2);
   *out = p;
   return CS_OK;
@@ -2070,9 +2239,23 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   const double m_total = (double)db->m_total;
   // ev0/ev1 bracket the whole histogram phase (K1 global + K1 SMEM + K1g) on this stream
   CS_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+  // fork: launches of the histogram phase rotate over the context stream and the side streams
+  // (CS_STREAMS = 1 keeps everything on the context stream)
+  const int nlaunch = (int)p->groups.size() + (p->ngitems > 0) + !p->generic_list.empty() + !p->waves.empty() +
+                      !p->blaunch.empty() + !p->swaves.empty();
+  const int nstreams = nlaunch > 1 ? std::max(1, std::min(1 + cs_ctx::NSIDE, env_int("CS_STREAMS", 4))) : 1;
+  int rr = 0;  // next stream of the rotation
+  auto pick = [&]() -> cudaStream_t {
+    const int s = rr++ % nstreams;
+    return s == 0 ? ctx->stream : ctx->side[s - 1];
+  };
+  if (nstreams > 1) {
+    CS_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    for (int i = 0; i + 1 < nstreams; ++i) CS_CUDA(cudaStreamWaitEvent(ctx->side[i], ctx->fork_ev, 0));
+  }
   if (p->ngitems > 0) {
     const int grid = std::min(2 * ctx->num_sms, p->ngitems);
-    k_hist_global<<<grid, 512, 0, ctx->stream>>>(p->d_q, p->d_items + p->nitems, p->ngitems,
+    k_hist_global<<<grid, 512, 0, pick()>>>(p->d_q, p->d_items + p->nitems, p->ngitems,
                                                  p->d_head + 1, dtab);
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
@@ -2084,7 +2267,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
       HistFn f = kHist[k - 1][path][nib];
       if (!f) return fail(CS_ERR_INVALID, "internal: no K1 variant for k=%d path=%d", k, path);
       const int grid = std::min(ctx->hist_ctas, G.count);
-      f<<<grid, CS_HIST_THREADS, ctx->hist_smem, ctx->stream>>>(
+      f<<<grid, CS_HIST_THREADS, ctx->hist_smem, pick()>>>(
           p->d_q, p->d_items + G.first, G.count, p->d_head + 2 + (int)g, dtab, p->d_done,
           (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev, flags, m_total);
       ctx->launches++;
@@ -2094,7 +2277,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   if (!p->generic_list.empty()) {
     dim3 grid((unsigned)std::min<int64_t>((db->m + 255) / 256, 1024),
               (unsigned)std::min<size_t>(p->generic_list.size(), 65535));
-    k_hist_generic<<<grid, 256, 0, ctx->stream>>>(p->d_q, p->d_generic_list, p->d_gvars, p->d_gstride,
+    k_hist_generic<<<grid, 256, 0, pick()>>>(p->d_q, p->d_generic_list, p->d_gvars, p->d_gstride,
                                                   db->cols, db->ld, db->m, dtab, (int)p->generic_list.size());
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
@@ -2103,43 +2286,73 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     // partition class: per wave, k_radix_part per digit count, then k_radix_count
     void* scr = nullptr;
     CS_TRY(ctx->scratch_get(23, p->rx_scratch, &scr));
-    CS_CUDA(cudaMemsetAsync(p->d_rhead, 0, sizeof(int) * p->waves.size(), ctx->stream));
+    const cudaStream_t ws = pick();  // waves share the scratch: one stream for all of them
+    CS_CUDA(cudaMemsetAsync(p->d_rhead, 0, sizeof(int) * p->waves.size(), ws));
     for (size_t w = 0; w < p->waves.size(); ++w) {
       const auto& wv = p->waves[w];
       for (const auto& L : wv.parts) {
         const int total = L.count * p->rx_nchunks;
         if (total == 0) continue;
         const int grid = std::min(total, 4 * ctx->num_sms);
-        kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ctx->stream>>>(p->d_rdesc + L.first, L.count,
+        kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ws>>>(p->d_rdesc + L.first, L.count,
                                                                          p->rx_nchunks, db->m, (char*)scr);
         ctx->launches++;
         CS_CUDA(cudaGetLastError());
       }
       if (wv.nitems > 0 && p->rx_nchunks > 0) {
         const int grid = std::min(wv.nitems, ctx->num_sms);
-        k_radix_count<<<grid, RC_THREADS, RC_SMEM, ctx->stream>>>(p->d_q, p->d_rdesc, p->d_ritems + wv.item0,
+        k_radix_count<<<grid, RC_THREADS, RC_SMEM, ws>>>(p->d_q, p->d_rdesc, p->d_ritems + wv.item0,
                                                                   wv.nitems, p->d_rhead + w, dtab, (const char*)scr);
         ctx->launches++;
         CS_CUDA(cudaGetLastError());
       }
     }
   }
+  if (!p->swaves.empty()) {
+    // spill class: per wave, k_spill_hist per digit count, then k_spill_count
+    void* scr = nullptr;
+    CS_TRY(ctx->scratch_get(24, p->sp_scratch, &scr));
+    const cudaStream_t ss = pick();  // waves share the scratch: one stream for all of them
+    CS_CUDA(cudaMemsetAsync(p->d_shead, 0, sizeof(int) * p->sp_heads, ss));
+    int hd = 0;
+    for (const auto& wv : p->swaves) {
+      for (const auto& L : wv.parts) {
+        const int grid = std::min(L.count, ctx->hist_ctas);
+        kSpillHist[L.k - 1]<<<grid, SP_THREADS, ctx->hist_smem, ss>>>(p->d_sdesc, p->d_sitems + L.first, L.count,
+                                                                      p->d_shead + hd++, dtab, (char*)scr);
+        ctx->launches++;
+        CS_CUDA(cudaGetLastError());
+      }
+      const int grid = std::min(wv.nitems, ctx->num_sms);
+      k_spill_count<<<grid, SP_THREADS, SP_COUNT_SMEM, ss>>>(p->d_sdesc, p->d_citems + wv.item0, wv.nitems,
+                                                            p->d_shead + hd++, dtab, (const char*)scr);
+      ctx->launches++;
+      CS_CUDA(cudaGetLastError());
+    }
+  }
   if (!p->blaunch.empty()) {
     // bitmap class: subset popcounts per digit count, then the in-place superset -> cell transform
-    CS_CUDA(cudaMemsetAsync(p->d_bhead, 0, sizeof(int) * BQ_MAXK, ctx->stream));
+    const cudaStream_t bs = pick();  // subset popcounts, then their in-place transform: one stream
+    CS_CUDA(cudaMemsetAsync(p->d_bhead, 0, sizeof(int) * BQ_MAXK, bs));
     for (size_t i = 0; i < p->blaunch.size(); ++i) {
       const auto& L = p->blaunch[i];
       const int per_sm = bq_smem_bytes(L.k) <= 100 * 1024 ? 2 : 1;
       const int grid = std::min(L.nitems, per_sm * ctx->num_sms);
-      kBitmapQ[L.k - 1]<<<grid, BQ_THREADS, bq_smem_bytes(L.k), ctx->stream>>>(
+      kBitmapQ[L.k - 1]<<<grid, BQ_THREADS, bq_smem_bytes(L.k), bs>>>(
           p->d_bdesc, p->d_bitems + L.item0, L.nitems, p->d_bhead + i, db->words, dtab);
       ctx->launches++;
       CS_CUDA(cudaGetLastError());
     }
     const int nb = (int)p->bdesc.size();
-    k_bitmap_mobius<<<(nb + 127) / 128, 128, 0, ctx->stream>>>(p->d_bdesc, nb, (uint32_t)db->m, dtab);
+    k_bitmap_mobius<<<(nb + 127) / 128, 128, 0, bs>>>(p->d_bdesc, nb, (uint32_t)db->m, dtab);
     ctx->launches++;
     CS_CUDA(cudaGetLastError());
+  }
+  if (nstreams > 1) {  // join
+    for (int i = 0; i + 1 < nstreams; ++i) {
+      CS_CUDA(cudaEventRecord(ctx->join_ev[i], ctx->side[i]));
+      CS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[i], 0));
+    }
   }
   for (auto& sq : p->sparse) CS_TRY(run_sparse(p, sq, flags, (double*)lb.dev, (double*)mb.dev, (int64_t*)nb.dev));
   CS_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

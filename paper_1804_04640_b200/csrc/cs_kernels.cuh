@@ -831,7 +831,10 @@ __device__ __forceinline__ void dispatch_global_rows(const QDesc& q, int64_t r0,
 // and the last segment to arrive (done counter) scores the merged table.
 enum : int { P_LANE16 = 0, P_PACK2 = 1, P_PACK4 = 2, P_ROWS = 3, P_HALF = 4, P_SLICE = 5, P_NARROW8 = 6,
               P_NARROW16 = 7 };
-constexpr int CS_HIST_THREADS = 1024;
+#ifndef CS_THREADS_N
+#define CS_THREADS_N 1024
+#endif
+constexpr int CS_HIST_THREADS = CS_THREADS_N;
 
 template <int K, int PATH, int NIB>
 __global__ void __launch_bounds__(CS_HIST_THREADS, 1)

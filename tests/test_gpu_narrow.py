@@ -52,13 +52,13 @@ def test_narrow_uniform(ctx, monkeypatch, capfd, m):
     ar = [16, 15, 13, 16, 8, 7, 9, 5]
     data = np.vstack([rng.integers(0, a, m) for a in ar]).astype(np.uint8)
     gdb = GpuDatabase.from_columns(ctx, data, ar)
-    # 16*15*13 = 3120 .. 16*15*13*16 = 49,920 (SMEM) | *8 = 399K (partition) ...
+    # 16*15*13 = 3120 .. 16*15*13*16 = 49,920 (SMEM) | *8 = 399K (spill / partition) ...
     qs = [(0, 1, 2, 5, 7), (0, 1, 2, 4, 7), (3, 2, 1, 0), (1, 3, 4, 5), (0, 3, 5, 6), (2, 3, 6, 7, 4),
           (0, 1, 3, 4), (5, 0, 1, 2, 6), (7, 6, 5, 4, 3, 2)]
     monkeypatch.setenv("CS_TRACE", "1")
     _check(gdb, data, ar, qs)
     cls = _classes(capfd)
-    assert cls["smem"] >= 4 and cls["partition"] >= 1
+    assert cls["smem"] >= 4 and cls["partition"] + cls["spill"] >= 1
     monkeypatch.setenv("CS_NARROW_SEG_ROWS", "65536")  # many segments per query
     monkeypatch.setenv("CS_SEG_MAX_ROWS", "65536")
     _check(gdb, data, ar, qs)
@@ -98,6 +98,7 @@ def test_narrow_off_matches_partition(ctx, monkeypatch):
     qs += [tuple(int(x) for x in rng.permutation(6)[:5]) + () for _ in range(4)]  # 32,768: SMEM
     qs += [(0, 1, 2, 3, 4, 5)[:6]]
     monkeypatch.setenv("CS_NARROW", "0")
+    monkeypatch.setenv("CS_SPILL", "0")
     _check(gdb, data, ar, qs)
     monkeypatch.setenv("CS_NARROW", "1")
     ar2 = [8, 8, 8, 8, 8, 3]
@@ -122,6 +123,7 @@ def test_narrow_multipass(ctx, monkeypatch, capfd, m):
     gdb = GpuDatabase.from_columns(ctx, data, ar)
     qs = [(0, 1, 2, 3, 4), (4, 3, 2, 1, 0), (0, 1, 2, 3, 5), (5, 0, 1, 2, 3), (1, 2, 3, 4, 5)]
     _check(gdb, data, ar, qs)  # 393,216 / 327,680 / 122,880 cells: 2 passes, 2 passes, 1
-    assert _classes(capfd)["partition"] == 0
+    c = _classes(capfd)
+    assert c["partition"] == 0 and c["spill"] == 0
     monkeypatch.setenv("CS_NARROW_PASS_SEG_ROWS", "65536")
     _check(gdb, data, ar, qs)

@@ -213,7 +213,8 @@ def _big_table_workload(m, nq=24, seed=7):
     return w, qs
 
 
-@pytest.mark.parametrize("env", [{}, {"CS_RADIX_CPI": "2", "CS_RADIX_MB": "1"}, {"CS_RADIX": "0"}])
+@pytest.mark.parametrize("env", [{}, {"CS_SPILL": "0"}, {"CS_SPILL": "0", "CS_RADIX_CPI": "2", "CS_RADIX_MB": "1"},
+                                 {"CS_SPILL": "0", "CS_RADIX": "0"}])
 def test_partition_class_big_tables(env):
     """Tables above SMEM capacity: the partition class (one counting-sort pass + SMEM group
     histograms), forced into many count items / one-query waves, and the slice / global
@@ -814,3 +815,38 @@ def test_query_batch_pipelined_chunks(ctx, outputs, monkeypatch):
     assert np.array_equal(one[0].view(np.uint32), otabs)
     assert np.array_equal(one[3], onnz)
     assert all(rel_close(a, b, 1e-9) for a, b in zip(one[1], oll))
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_query_batch_score_only_chunks(ctx, chunks, monkeypatch):
+    """The score-only one-shot path (no tables): one plan and forced chunking, raw C ABI and the
+    drop-in GpuStrategy.query_batch with and without tables, against the dense oracle."""
+    from paper_1804_04640_b200.database import Database, QuerySpec
+    from paper_1804_04640_b200.engine import encode_queries
+    from paper_1804_04640_b200.harness import GpuStrategy
+
+    rng = np.random.default_rng(77)
+    n, m = 16, 90_001
+    arities = rng.integers(2, 6, size=n).astype(np.int32)
+    cols = np.stack([rng.integers(0, a, size=m) for a in arities]).astype(np.uint8)
+    queries = [tuple(int(v) for v in rng.choice(n, size=int(rng.integers(1, 6)), replace=False))
+               for _ in range(3000)]
+    monkeypatch.setenv("CS_QB_CHUNKS", str(chunks))
+    monkeypatch.setenv("CS_QB_SCORE_MIN", "1")
+    gdb = GpuDatabase.from_columns(ctx, cols, arities)
+    off, flat = encode_queries(queries)
+    ll, mi, nz = np.zeros(len(queries)), np.zeros(len(queries)), np.zeros(len(queries), dtype=np.int64)
+    gdb.query_batch(off, flat, 0, loglik=ll, mi=mi, nnz=nz)
+    _, _, oll, omi, onnz = O.dense_tables(cols, arities, queries, want_tables=False)
+    assert np.array_equal(nz, onnz)
+    assert all(rel_close(a, b, 1e-9) for a, b in zip(ll, oll))
+    assert np.all(np.abs(mi - omi) <= 1e-9 * (np.abs(oll) + 1) / m + 1e-15)
+    strat = GpuStrategy(Database(cols.astype(np.int32), [int(a) for a in arities]))
+    specs = [QuerySpec(q[0], tuple(q[1:])) for q in queries]
+    a = strat.query_batch(specs, loglik=True, mi=True, nnz=True)
+    b = strat.query_batch(specs, loglik=True, mi=True, nnz=True, tables=True)
+    assert np.array_equal(a["nnz"], onnz) and np.array_equal(b["nnz"], onnz)
+    assert all(rel_close(x, y, 1e-12) for x, y in zip(a["loglik"], b["loglik"]))
+    assert all(rel_close(x, y, 1e-9) for x, y in zip(a["loglik"], oll))
+    otabs = O.dense_tables(cols, arities, queries)[0]
+    assert np.array_equal(b["tables"], otabs)

@@ -28,16 +28,18 @@ ref = None
 for env in settings:
     for k, v in env.items():
         os.environ[k] = v
-    plan = QueryPlan(gdb, w.queries, 1)
+    bench_like = os.environ.get("CFG5_BENCH_OUTPUTS") == "1"  # bench.py's cfg5 outputs: LL + MI, no tables flag
+    plan = QueryPlan(gdb, w.queries, 0 if bench_like else 1)
     tabs = torch.empty(plan.total_cells, dtype=torch.int32, device="cuda")
     ll = torch.empty(plan.nq, dtype=torch.float64, device="cuda")
-    plan.execute(tables=tabs, loglik=ll)
+    mi = torch.empty(plan.nq, dtype=torch.float64, device="cuda") if bench_like else None
+    plan.execute(tables=tabs, loglik=ll, mi=mi)
     ts, ks = [], []
     for _ in range(3):
         flush.fill_(1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        plan.execute(tables=tabs, loglik=ll)
+        plan.execute(tables=tabs, loglik=ll, mi=mi)
         b.record(stream)
         b.synchronize()
         ts.append(a.elapsed_time(b))
