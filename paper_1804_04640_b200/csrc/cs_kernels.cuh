@@ -321,6 +321,16 @@ __device__ __forceinline__ void for_words(const uint32_t (&x)[K][4], WordFn f) {
   }
 }
 
+// Calls run(std::integral_constant<int, NB>) with the compile-time byte-lane digit count the
+// query's nbyte allows: every digit (NB = K), 3, 2, or 0 = decide per digit at run time.
+template <int K, class Run>
+__device__ __forceinline__ void dispatch_nbyte(int nbyte, Run run) {
+  if (nbyte >= K) run(std::integral_constant<int, K>{});
+  else if (K > 3 && nbyte >= 3) run(std::integral_constant<int, (K > 3 ? 3 : K)>{});
+  else if (K > 2 && nbyte == 2) run(std::integral_constant<int, (K > 2 ? 2 : K)>{});
+  else run(std::integral_constant<int, 0>{});
+}
+
 template <int K, int NIB>
 __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int64_t r1,
                                                  uint32_t* sh) {
@@ -340,39 +350,46 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
   char* shb = reinterpret_cast<char*>(sh);
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + RPV - 1) / RPV;
-  auto word = [&](const uint32_t (&w)[K]) {
-    uint32_t a8 = w[0];
+  // NB = digits combined in byte lanes, fixed at compile time (NB = 0: the runtime nbyte,
+  // every digit's byte-lane and 16-bit-lane forms both issued under predicates).  Any
+  // NB <= nbyte is valid: later digits just take the 16-bit lanes.
+  auto run = [&](auto nbc) {
+    constexpr int NB = decltype(nbc)::value;
+    auto word = [&](const uint32_t (&w)[K]) {
+      uint32_t a8 = w[0];
 #pragma unroll
-    for (int v = 1; v < K; ++v)
-      if (v < nbyte) a8 += w[v] * st[v];
-    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+      for (int v = 1; v < K; ++v)
+        if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
+      uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+      uint32_t hi = __byte_perm(a8, 0u, 0x4342);
 #pragma unroll
-    for (int v = 1; v < K; ++v) {
-      if (v >= nbyte) {
-        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
-        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      for (int v = 1; v < K; ++v) {
+        if (NB ? v >= NB : v >= nbyte) {
+          lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+          hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+        }
+      }
+      lo = lo * scale + rep_pair;
+      hi = hi * scale + rep_pair;
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
+    };
+    auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+    if (q.stages >= 3) {
+      const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+      if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+      else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
+    } else {
+      for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+        uint32_t a[K][4];
+        load_vec16<K>(a, rowp + (vi << 4), co);
+        cnt(a);
       }
     }
-    lo = lo * scale + rep_pair;
-    hi = hi * scale + rep_pair;
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
   };
-  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
-  if (q.stages >= 3) {
-    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
-    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
-    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
-  } else {
-    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
-      uint32_t a[K][4];
-      load_vec16<K>(a, rowp + (vi << 4), co);
-      cnt(a);
-    }
-  }
+  dispatch_nbyte<K>(nbyte, run);
   const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
   if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
@@ -523,37 +540,41 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
   char* rbase = reinterpret_cast<char*>(sh) + rep4;
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + RPV - 1) / RPV;
-  auto word = [&](const uint32_t (&w)[K]) {
-    uint32_t a8 = w[0];
+  auto run = [&](auto nbc) {
+    constexpr int NB = decltype(nbc)::value;  // as in hist_smem_lane16
+    auto word = [&](const uint32_t (&w)[K]) {
+      uint32_t a8 = w[0];
 #pragma unroll
-    for (int v = 1; v < K; ++v)
-      if (v < nbyte) a8 += w[v] * st[v];
-    uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-    uint32_t hi = __byte_perm(a8, 0u, 0x4342);
+      for (int v = 1; v < K; ++v)
+        if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
+      uint32_t lo = __byte_perm(a8, 0u, 0x4140);
+      uint32_t hi = __byte_perm(a8, 0u, 0x4342);
 #pragma unroll
-    for (int v = 1; v < K; ++v) {
-      if (v >= nbyte) {
-        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
-        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      for (int v = 1; v < K; ++v) {
+        if (NB ? v >= NB : v >= nbyte) {
+          lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+          hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+        }
+      }
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo & 0xffffu) * scale), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo >> 16) * scale), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi & 0xffffu) * scale), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi >> 16) * scale), 1u);
+    };
+    auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
+    if (q.stages >= 3) {
+      const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
+      if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
+      else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
+    } else {
+      for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+        uint32_t a[K][4];
+        load_vec16<K>(a, rowp + (vi << 4), co);
+        cnt(a);
       }
     }
-    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo & 0xffffu) * scale), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo >> 16) * scale), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi & 0xffffu) * scale), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi >> 16) * scale), 1u);
   };
-  auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
-  if (q.stages >= 3) {
-    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sh) + q.stage_off;
-    if (q.stages >= 4) staged_rows<K, 4>(rowp, co, nvec, ring, cnt);
-    else staged_rows<K, 3>(rowp, co, nvec, ring, cnt);
-  } else {
-    for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
-      uint32_t a[K][4];
-      load_vec16<K>(a, rowp + (vi << 4), co);
-      cnt(a);
-    }
-  }
+  dispatch_nbyte<K>(nbyte, run);
   const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
   if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(reinterpret_cast<uint32_t*>(rbase), (uint32_t)pad);
@@ -688,7 +709,11 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
   const int64_t nvec = (nrows + 31) >> 5;
   constexpr uint32_t PER = 32 / BITS, MASK = (1u << BITS) - 1u;
   // RANGED: a pass over part of the table (rows outside [lo, lo + C) skipped); the single-pass
-  // loop has no range test (every joint index is a cell)
+  // loop has no range test (every joint index is a cell).  The counter bump is hand-scheduled:
+  // increment = 1 << (BITS * lane) by one wrapping funnel shift of idx * BITS, word address =
+  // idx * BITS / 8 rounded down to 4, predicated atom.shared (no branch), and the wrap test
+  // "(~old & (inc * MASK)) == 0" on the word the atomic returned.
+  const uint32_t tab = (uint32_t)__cvta_generic_to_shared(sh);
   auto run = [&](auto ranged) {
     constexpr bool RANGED = decltype(ranged)::value;
     for (int64_t vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
@@ -699,21 +724,33 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           // the 4 rows of one word view: all atomics issued before any wrap test reads a result
-          uint32_t idx[4], old[4];
+          uint32_t idx[4], old[4], inc[4];
           nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             if (RANGED) idx[t] -= lo;
-            old[t] = (!RANGED || idx[t] < C) ? atomicAdd(&sh[idx[t] / PER], 1u << ((idx[t] % PER) * BITS)) : 0u;
+            asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(inc[t]) : "r"(idx[t] * (uint32_t)BITS));
+            const uint32_t addr = tab + ((idx[t] * (uint32_t)(BITS / 8)) & ~3u);
+            if (RANGED) {
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.lt.u32 p, %3, %4;\n\t"
+                  "mov.u32 %0, 0;\n\t"
+                  "@p atom.shared.add.u32 %0, [%1], %2;\n\t}"
+                  : "=r"(old[t])
+                  : "r"(addr), "r"(inc[t]), "r"(idx[t]), "r"(C)
+                  : "memory");
+            } else {
+              asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old[t]) : "r"(addr), "r"(inc[t]) : "memory");
+            }
           }
           bool wrap = false;
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
-            wrap |= (!RANGED || idx[t] < C) && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK;
+          for (int t = 0; t < 4; ++t) wrap |= (~old[t] & (inc[t] * MASK)) == 0u;
           if (wrap) {
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-              if ((!RANGED || idx[t] < C) && ((old[t] >> ((idx[t] % PER) * BITS)) & MASK) == MASK)
+              if ((~old[t] & (inc[t] * MASK)) == 0u)
                 narrow_fix<BITS>(old[t], idx[t] % PER, idx[t] / PER * PER, C, gtab);
           }
         }
