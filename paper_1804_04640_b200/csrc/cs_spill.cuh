@@ -1,4 +1,4 @@
-// cs_spill.cuh -- K1s, the spill class: joint tables up to ~3x one SM's shared memory
+// cs_spill.cuh -- K1sp, the spill class: joint tables up to ~3x one SM's shared memory
 // (225K .. ~600K cells), between the narrow-counter SMEM class and the partition class.
 //
 // The reference's radix strategy partitions ALL rows before it counts any (radix.py:33-79).
@@ -109,9 +109,23 @@ __device__ __forceinline__ void spill_rows(const uint32_t (&x)[K][4], const uint
         if (SLOW) {
           if (out) atomicAdd(gtab + idx[t], 1u);
         } else {
-          const uint32_t mask = __ballot_sync(0xffffffffu, out);
-          if (out) reg[cur + __popc(mask & lt)] = idx[t];
-          cur += __popc(mask);
+          // rank among the warp's spilled rows of this slot, one predicated 4-byte store (no
+          // branch), cursor advanced by the slot's count
+          uint32_t n;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t.reg .b32 m, r;\n\t.reg .b64 a;\n\t"
+              "setp.ne.u32 p, %4, 0;\n\t"
+              "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+              "and.b32 r, m, %3;\n\t"
+              "popc.b32 r, r;\n\t"
+              "add.u32 r, r, %2;\n\t"
+              "mad.wide.u32 a, r, 4, %1;\n\t"
+              "@p st.global.u32 [a], %5;\n\t"
+              "popc.b32 %0, m;\n\t}"
+              : "=r"(n)
+              : "l"(reg), "r"(cur), "r"(lt), "r"((uint32_t)out), "r"(idx[t])
+              : "memory");
+          cur += n;
         }
       }
     }

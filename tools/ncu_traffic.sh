@@ -9,7 +9,7 @@ OUT=${OUT:-gpurun_out/ncu}
 mkdir -p $OUT
 case $cfg in
   cfg4) K='regex:k_sel|k_itemsets|k_pmt' ;;
-  *) K='regex:k_hist|k_radix|k_bitmap_query|k_score|k_family' ;;
+  *) K='regex:k_hist|k_radix|k_spill|k_bitmap_query|k_bitmap_mobius|k_score|k_family' ;;
 esac
 ncu --cache-control none --clock-control none --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     -k "$K" --log-file $OUT/${cfg}_launches.csv python bench.py --config $cfg --steps 1 --warmup 3 --no-cpu-baseline "$@" \
