@@ -177,7 +177,7 @@ int cs_plan_compact(cs_plan* plan, const uint32_t* tables, const int64_t* out_of
                     int64_t* cell_idx, int64_t* n_ijk, int64_t* n_ij);
 int cs_plan_destroy(cs_plan* plan);
 /* create + execute + destroy.  Batches of >= ~4K queries are split into 2-4 chunks (chunk j a
- * 4^j share, first chunk >= 2K queries; env CS_QB_CHUNKS / CS_QB_GROWTH / CS_QB_MIN_CHUNK
+ * 2^j share, first chunk >= 1.4K queries; env CS_QB_CHUNKS / CS_QB_GROWTH / CS_QB_MIN_CHUNK
  * override) whose host planning overlaps the previous chunk's kernels; outputs land at the same
  * offsets as one plan's (tables in query order, one entry per query in loglik / mi / nnz).
  * The whole batch is validated before the first chunk launches (errors name the query's index

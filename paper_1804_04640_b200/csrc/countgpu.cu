@@ -2473,7 +2473,7 @@ static int query_batch_pipelined(cs_db* db, int32_t nq, const int32_t* var_off, 
   if (!var_off || !vars) return fail(CS_ERR_INVALID, "cs_plan_create: NULL query arrays");
   nchunks = std::min(nchunks, 8);
   // chunk j holds a growth^j share of the batch (growth 4: 1/5 + 4/5, 1/21 + 4/21 + 16/21, ...)
-  const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 4), 1), 8);
+  const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 2), 1), 8);
   std::vector<int64_t> gp(nchunks + 1, 1);
   for (int j = 1; j <= nchunks; ++j) gp[j] = gp[j - 1] * growth;
   int64_t wsum = 0;
@@ -2543,18 +2543,19 @@ extern "C" int cs_query_batch(cs_db* db, int32_t nq, const int32_t* var_off, con
   const bool trace = env_int("CS_TRACE", 0) != 0;
   // big batches: plan chunk j+1 on the host while chunk j's kernels run (chunk sizes double,
   // so each chunk's execution covers the next chunk's planning; only the first plan is exposed).
-  // Chunk j holds a CS_QB_GROWTH^j share; a first chunk below ~2K queries loses more to K1
-  // launch tails than its planning costs (cfg2 e2e, 10K queries: one plan 4.08 ms; 2 chunks at
-  // growth 2/3/4: 3.89/3.85/3.81; 3 chunks at growth 2/3/4: 4.13/4.01/3.93; cfg3, 289K
-  // queries: 30.7 -> 24.5-24.7 ms for 3-5 chunks at growth 2-3)
+  // Chunk j holds a CS_QB_GROWTH^j share; a first chunk below ~1.4K queries loses more to K1
+  // launch tails than its planning costs.  Round 1 kernels (cfg2 e2e, 10K queries): one plan
+  // 4.08 ms; 2 chunks at growth 2/3/4: 3.89/3.85/3.81.  Round 2 kernels are ~20% faster, a chunk
+  // covers less planning, and growth 2 wins: cfg2 growth 2 (3-4 chunks) 3.19-3.24 ms against
+  // growth 4 (2 chunks) 3.28-3.42; cfg3 (74.5K subsets) 21.9-22.3 against 23.4-29.4 ms.
   // Score-only batches of cfg2's size lose (LL-only 10K queries: 4.20 ms one plan, 4.62 ms
   // chunked; the kernels skip the table stores, so chunk j no longer covers chunk j+1's plan):
   // they are chunked only from 32K queries (cfg3's 289K LL+MDL batch gains 30.7 -> 25 ms).
   int nchunks = env_int("CS_QB_CHUNKS", 0);
   if (nchunks <= 0 && !tables && nq < env_int("CS_QB_SCORE_MIN", 32768)) nchunks = 1;
   if (nchunks <= 0) {
-    const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 2000), 1);
-    const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 4), 1), 8);
+    const int64_t min_chunk = std::max(env_int("CS_QB_MIN_CHUNK", 1400), 1);
+    const int64_t growth = std::min(std::max(env_int("CS_QB_GROWTH", 2), 1), 8);
     int64_t w = 1, wsum = 1;
     nchunks = 1;
     while (nchunks < 4) {
