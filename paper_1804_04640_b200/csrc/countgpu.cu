@@ -1659,7 +1659,7 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       else cudaGetLastError();
       const int W = (int)std::max<size_t>(1, std::min<size_t>(budget / slot, rq.size()));
       p->rx_scratch = slot * (size_t)W;
-      const int64_t cpi = std::max(1, env_int("CS_RADIX_CPI", 2048));
+      const int64_t cpi = std::max(1, env_int("CS_RADIX_CPI", 2048 * (8192 / RX_CH)));  // 16M rows per count item
       const int64_t G = std::max<int64_t>(1, (nchunks + cpi - 1) / cpi);
       const int64_t cper = std::max<int64_t>(1, (nchunks + G - 1) / G);
       for (size_t w0 = 0; w0 < rq.size(); w0 += (size_t)W) {
@@ -2220,6 +2220,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
   CS_CUDA(cudaSetDevice(ctx->device));
   if (p->nq == 0) return CS_OK;
   uint32_t flags = p->flags;
+  if (env_int("CS_NARROW_FAST", 1) == 0) flags |= F_NARROW_EXACT;
   if (loglik) flags |= F_LOGLIK;
   if (mi) flags |= F_MI;
   if (nnz) flags |= F_NNZ;
@@ -2293,7 +2294,7 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
       for (const auto& L : wv.parts) {
         const int total = L.count * p->rx_nchunks;
         if (total == 0) continue;
-        const int grid = std::min(total, 4 * ctx->num_sms);
+        const int grid = std::min(total, (1024 / RX_THREADS) * ctx->num_sms);
         kRadixPart[L.k - 1]<<<grid, RX_THREADS, RX_SMEM, ws>>>(p->d_rdesc + L.first, L.count,
                                                                          p->rx_nchunks, db->m, (char*)scr);
         ctx->launches++;

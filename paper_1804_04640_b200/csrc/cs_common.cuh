@@ -67,6 +67,7 @@ enum : uint32_t {
   F_NNZ = 0x8u,
   F_PARTIAL = 0x10u,
   F_NLOGN = 0x20u,  // the loglik output receives sum_cells n ln n (joint "entropy numerator")
+  F_NARROW_EXACT = 0x100u,  // internal (CS_NARROW_FAST=0): narrow classes skip their optimistic pass
 };
 
 // Counter-based generator (twin: oracle/gen_twin.py).  splitmix64 finaliser.

@@ -695,7 +695,10 @@ __device__ __forceinline__ void nib_joint4(const uint32_t (&x)[K][4], int j, int
 
 // One pass counts the cells [lo, lo + C) (several passes over an L2-resident row segment when
 // the table exceeds one SM even with 8-bit counters); rows outside the range are skipped.
-template <int K, int BITS>
+// FAST: the optimistic form -- non-returning red.shared, no wrap test, no padding fix-up; the
+// caller verifies afterwards that no counter wrapped (k_hist) and reruns the exact form if one
+// did.  Whole-table passes only.
+template <int K, int BITS, bool FAST = false>
 __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int64_t r1, uint32_t* sh,
                                                  uint32_t* gtab, uint32_t lo, uint32_t C) {
   const uint8_t* rowp = q.base + (r0 >> 1);
@@ -731,7 +734,10 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
             if (RANGED) idx[t] -= lo;
             asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(inc[t]) : "r"(idx[t] * (uint32_t)BITS));
             const uint32_t addr = tab + ((idx[t] * (uint32_t)(BITS / 8)) & ~3u);
-            if (RANGED) {
+            if (FAST) {
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(inc[t]) : "memory");
+              old[t] = 0u;
+            } else if (RANGED) {
               asm volatile(
                   "{\n\t.reg .pred p;\n\t"
                   "setp.lt.u32 p, %3, %4;\n\t"
@@ -744,6 +750,7 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
               asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old[t]) : "r"(addr), "r"(inc[t]) : "memory");
             }
           }
+          if (FAST) continue;
           bool wrap = false;
 #pragma unroll
           for (int t = 0; t < 4; ++t) wrap |= (~old[t] & (inc[t] * MASK)) == 0u;
@@ -757,8 +764,9 @@ __device__ __forceinline__ void hist_smem_narrow(const QDesc& q, int64_t r0, int
       }
     }
   };
-  if (lo == 0 && C == q.cells) run(std::false_type{});
+  if (FAST || (lo == 0 && C == q.cells)) run(std::false_type{});
   else run(std::true_type{});
+  if (FAST) return;
   const int64_t pad = (nvec << 5) - nrows;  // padding rows (zero nibbles) counted into cell 0
   if (lo == 0 && pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(gtab, (uint32_t)pad);
@@ -911,14 +919,45 @@ __global__ void __launch_bounds__(CS_HIST_THREADS, 1)
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
     if (threadIdx.x < 64) s_marg[threadIdx.x] = 0u;
     __syncthreads();
-    if (PATH == P_LANE16) hist_smem_lane16<K, NIB>(q, wi.r0, wi.r1, sh);
-    else if (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
-    else if (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
-    else if (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
-    else if (PATH == P_SLICE)
+    if constexpr (PATH == P_LANE16) hist_smem_lane16<K, NIB>(q, wi.r0, wi.r1, sh);
+    else if constexpr (PATH == P_PACK2) hist_smem_packed<(K <= 5 ? K : 5), 2, NIB>(q, wi.r0, wi.r1, sh);
+    else if constexpr (PATH == P_PACK4) hist_smem_packed<(K <= 5 ? K : 5), 4, NIB>(q, wi.r0, wi.r1, sh);
+    else if constexpr (PATH == P_HALF) hist_smem_half<K, NIB>(q, wi.r0, wi.r1, sh);
+    else if constexpr (PATH == P_SLICE)
       hist_smem_slice<(K >= 2 ? K : 2), NIB>(q, wi.r0, wi.r1, sh, (uint32_t)wi.slice, (uint32_t)wi.nsl);
-    else if (PATH == P_NARROW8) hist_smem_narrow<K, 8>(q, wi.r0, wi.r1, sh, tables + q.table_off + plo, plo, C);
-    else if (PATH == P_NARROW16) hist_smem_narrow<K, 16>(q, wi.r0, wi.r1, sh, tables + q.table_off + plo, plo, C);
+    else if constexpr (NARROW) {
+      // Optimistic pass first (whole-table passes): plain red.shared, no wrap tests.  A word's
+      // counter sum equals its increments exactly when none of its counters wrapped (a wrap
+      // turns 2^BITS of one lane into 1 of the next, or into nothing), so "sum of all counters
+      // == rows counted" proves the table; otherwise it is zeroed and counted again by the exact
+      // form with its wrap repairs.
+      constexpr int NB_ = PATH == P_NARROW8 ? 8 : 16;
+      uint32_t* gt = tables + q.table_off + plo;
+      bool exact = q.npass > 1 || (flags & F_NARROW_EXACT);
+      if (!exact) {
+        hist_smem_narrow<K, NB_, true>(q, wi.r0, wi.r1, sh, gt, 0u, C);
+        __syncthreads();
+        unsigned long long part = 0ull;
+        for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
+          const uint32_t w = sh[i];
+          part += NB_ == 8 ? __dp4a(w, 0x01010101u, 0u) : (w & 0xffffu) + (w >> 16);
+        }
+        const unsigned long long tot = block_sum_u64(part, ss.redu);
+        const int64_t nrows = wi.r1 - wi.r0, nvec = (nrows + 31) >> 5;
+        if (threadIdx.x == 0) {
+          s_last = tot != (unsigned long long)(nvec << 5);
+          // padding rows (zero nibbles) of the last vector were counted into cell 0
+          if (!s_last && (nvec << 5) > nrows) atomicSub(gt, (uint32_t)((nvec << 5) - nrows));
+        }
+        __syncthreads();
+        exact = s_last != 0;
+        if (exact) {
+          for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) sh[i] = 0u;
+          __syncthreads();
+        }
+      }
+      if (exact) hist_smem_narrow<K, NB_>(q, wi.r0, wi.r1, sh, gt, plo, C);
+    }
     else hist_smem_rows16<K, NIB>(q, wi.r0, wi.r1, sh);
     __syncthreads();
     auto rep_sum = [&](uint32_t c) -> uint32_t {

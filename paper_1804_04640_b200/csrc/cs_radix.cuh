@@ -7,10 +7,10 @@
 // with an SMEM histogram.  This replaces RED.ADD into L2-resident global tables (one L2 atomic
 // per row) and the slice class (columns re-read once per slice) for tables of 56K..16M cells.
 //
-//   k_radix_part<K>   one chunk of RX_CH rows per CTA iteration: joint index of every row
+//   k_radix_part<K>   one chunk of RX_CH (4096) rows per CTA iteration: joint index of every row
 //                     from the 4-bit columns (16-bit SIMD lanes), SMEM histogram of the bucket
 //                     ids (idx >> bb), exclusive scan, counting-sort scatter of the low 15 bits
-//                     of idx into an SMEM stage, one coalesced 32 KB store of the stage plus the
+//                     of idx into an SMEM stage, one coalesced store of the stage (8 KB) plus the
 //                     chunk's bucket offsets.  HBM per row: K/2 B read + 2 B written.
 //   k_radix_count     (query, 32K-cell group, chunk range) items: each lane streams the run of
 //                     one chunk that falls in the group (buckets are sorted inside a chunk, and
@@ -22,10 +22,15 @@
 
 namespace cs {
 
-constexpr int RX_THREADS = 256;
+#ifndef CS_RX_THREADS_N
+#define CS_RX_THREADS_N 128
+#endif
+constexpr int RX_THREADS = CS_RX_THREADS_N;  // 1024 / RX_THREADS CTAs per SM (128: 8 CTAs whose barriers
+                                             // sync 4 warps each, 252 against 265 us per k = 8 query at 256)
 constexpr int RX_CH = RX_THREADS * 32;  // rows per chunk: one 16-B nibble vector per thread and column
 constexpr int RX_GROUP_BITS = 15;       // cells per count group (128 KB SMEM table)
-constexpr int RX_MAX_NB = 512;          // partition buckets per query (2 per k_radix_part thread)
+constexpr int RX_MAX_NB = 512;          // partition buckets per query
+constexpr int RX_NBPT = RX_MAX_NB / RX_THREADS;  // buckets scanned per k_radix_part thread
 constexpr int RX_SMEM = RX_CH * 4 + RX_CH * 2 + (RX_MAX_NB + 1) * 4;  // 4 CTAs per SM
 constexpr int RC_THREADS = 1024;
 constexpr int RC_DUMMY = 1 << RX_GROUP_BITS;          // counter for entries outside a run
@@ -117,7 +122,7 @@ __device__ __forceinline__ void radix_rows(const uint32_t (&x)[K][4], const uint
 }
 
 template <int K>
-__global__ void __launch_bounds__(RX_THREADS, 4)
+__global__ void __launch_bounds__(RX_THREADS, 1024 / RX_THREADS)
     k_radix_part(const RDesc* __restrict__ rd, int nrq, int nchunks, int64_t m, char* __restrict__ scratch) {
   extern __shared__ uint32_t rsm[];
   uint32_t* sidx = rsm;                                        // [32][RX_THREADS] joint indices
@@ -187,10 +192,15 @@ __global__ void __launch_bounds__(RX_THREADS, 4)
     have = rq2 == rq;
     if (have) load_vectors(x, base, coff, (int64_t)c2 * RX_CH + (int64_t)tid * 32);
     __syncthreads();
-    // exclusive scan of the bucket counts, two buckets per thread; the dummy bucket nb goes last
-    const uint32_t ca = 2 * tid < nb ? cnt[2 * tid] : 0u;
-    const uint32_t cb = 2 * tid + 1 < nb ? cnt[2 * tid + 1] : 0u;
-    const uint32_t mine = ca + cb;
+    // exclusive scan of the bucket counts, RX_NBPT consecutive buckets per thread; the dummy
+    // bucket nb goes last
+    uint32_t cv[RX_NBPT];
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int u = 0; u < RX_NBPT; ++u) {
+      cv[u] = RX_NBPT * tid + u < nb ? cnt[RX_NBPT * tid + u] : 0u;
+      mine += cv[u];
+    }
     uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -206,15 +216,15 @@ __global__ void __launch_bounds__(RX_THREADS, 4)
       if (w2 < warp) wpre += t;
       nstaged += t;
     }
-    const uint32_t excl = incl - mine + wpre;
+    uint32_t excl = incl - mine + wpre;
     int32_t* co = choff + (int64_t)c * (nb + 1);
-    if (2 * tid < nb) {
-      cnt[2 * tid] = excl;
-      co[2 * tid] = (int32_t)excl;
-    }
-    if (2 * tid + 1 < nb) {
-      cnt[2 * tid + 1] = excl + ca;
-      co[2 * tid + 1] = (int32_t)(excl + ca);
+#pragma unroll
+    for (int u = 0; u < RX_NBPT; ++u) {
+      if (RX_NBPT * tid + u < nb) {
+        cnt[RX_NBPT * tid + u] = excl;
+        co[RX_NBPT * tid + u] = (int32_t)excl;
+      }
+      excl += cv[u];
     }
     if (tid == 0) {
       cnt[nb] = nstaged;

@@ -62,12 +62,18 @@ def test_narrow_uniform(ctx, monkeypatch, capfd, m):
     monkeypatch.setenv("CS_NARROW_SEG_ROWS", "65536")  # many segments per query
     monkeypatch.setenv("CS_SEG_MAX_ROWS", "65536")
     _check(gdb, data, ar, qs)
+    monkeypatch.setenv("CS_NARROW_FAST", "0")  # no optimistic pass: the exact form alone
+    _check(gdb, data, ar, qs)
 
 
+@pytest.mark.parametrize("fast", ["1", "0"])
 @pytest.mark.parametrize("skew", ["constant", "four_lanes", "two_cells_far"])
-def test_narrow_wraps(ctx, monkeypatch, skew):
+def test_narrow_wraps(ctx, monkeypatch, skew, fast):
     """Counters wrap many times: one constant cell (carry out of lane 3 / the high half), rows
-    cycling through the 4 lanes of one word (carries through every lane), two hot cells."""
+    cycling through the 4 lanes of one word (carries through every lane), two hot cells.  With
+    the optimistic pass on (fast = 1) its counter-sum check must catch every one of these and
+    fall back to the exact form."""
+    monkeypatch.setenv("CS_NARROW_FAST", fast)
     m = 3_000_017
     ar = [16, 16, 16, 13]  # 53,248 cells: 32-bit class; with a 5th digit -> narrow
     ar5 = ar + [3]
