@@ -1,6 +1,6 @@
 #!/bin/bash
-# round 2 session 5: full GPU suite, bench lines of every config, reference arm, ncu launch lists (traffic)
-O=gpurun_out/s5a; mkdir -p $O
+# round 2 session 5 (final): full GPU suite, bench lines of every config, reference arm, ncu launch lists (traffic)
+O=gpurun_out/s5z; mkdir -p $O
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 3000 python -m pytest tests -m gpu -x -q --durations=15 > $O/gpu_tests.txt 2>&1
 tail -3 $O/gpu_tests.txt
