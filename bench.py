@@ -215,7 +215,8 @@ def host_columns(w, variables=None, rows=None):
 
 OUTPUTS = {"cfg1": "tables+loglik", "cfg2": "tables", "cfg3": "loglik+mdl", "cfg4": "pair+triple supports",
            "cfg5": "loglik+mi"}
-L2_NOTE = "GPU arm: L2 flushed (256 MB write) before every timed step"
+L2_NOTE = ("GPU arm: L2 NOT flushed (CS_BENCH_NOFLUSH=1, diagnostic run)" if os.environ.get("CS_BENCH_NOFLUSH") == "1"
+           else "GPU arm: L2 flushed (256 MB write) before every timed step")
 
 
 def arm_config(config: str, w, units: int) -> dict:
@@ -867,7 +868,8 @@ def run_ours(args, world, rank, local):
     kernel_ms = []
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.fill_(i)  # evict the database from L2 before every timed step (untimed)
+            if os.environ.get("CS_BENCH_NOFLUSH") != "1":  # diagnostic only: the line then says so
+                flush.fill_(i)  # evict the database from L2 before every timed step (untimed)
             starts[i].record(stream)
             r.step()
             ends[i].record(stream)
