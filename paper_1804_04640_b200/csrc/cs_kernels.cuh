@@ -346,7 +346,6 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
   const int rlog = q.rlog;
   const uint32_t scale = 4u << rlog;
   const uint32_t rep4 = (threadIdx.x & ((1u << rlog) - 1u)) * 4u;
-  const uint32_t rep_pair = rep4 | (rep4 << 16);
   char* shb = reinterpret_cast<char*>(sh);
   const int64_t nrows = r1 - r0;
   const int64_t nvec = (nrows + RPV - 1) / RPV;
@@ -369,12 +368,12 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
           hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
         }
       }
-      lo = lo * scale + rep_pair;
-      hi = hi * scale + rep_pair;
-      atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo & 0xffffu)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(shb + (lo >> 16)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi & 0xffffu)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(shb + (hi >> 16)), 1u);
+      // one IDP.2A per row: (16-bit lane) * 4R + 4 * replica, instead of an IMAD per lane pair
+      // plus a LOP3 / SHF extract per row on the saturated ALU pipe (4R <= 128 fits the byte)
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp2a_lo(lo, scale, rep4)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp2a_lo(lo, scale << 8, rep4)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp2a_lo(hi, scale, rep4)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp2a_lo(hi, scale << 8, rep4)), 1u);
     };
     auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
     if (q.stages >= 3) {
@@ -556,10 +555,10 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
           hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
         }
       }
-      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo & 0xffffu) * scale), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (lo >> 16) * scale), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi & 0xffffu) * scale), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(rbase + (hi >> 16) * scale), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(lo, scale, 0u)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(lo, scale << 8, 0u)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(hi, scale, 0u)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(hi, scale << 8, 0u)), 1u);
     };
     auto cnt = [&](const uint32_t (&x)[K][4]) { for_words<K, NIB>(x, word); };
     if (q.stages >= 3) {
