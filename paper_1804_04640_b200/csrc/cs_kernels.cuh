@@ -359,6 +359,15 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
 #pragma unroll
       for (int v = 1; v < K; ++v)
         if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
+      if constexpr (NB == K) {
+        // every digit in byte lanes (C <= 256): one IDP.4A per row picks the row's byte,
+        // scales it by 4R and adds the replica offset -- no split into 16-bit lanes at all
+        atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale, rep4)), 1u);
+        atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale << 8, rep4)), 1u);
+        atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale << 16, rep4)), 1u);
+        atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale << 24, rep4)), 1u);
+        return;
+      }
       uint32_t lo = __byte_perm(a8, 0u, 0x4140);
       uint32_t hi = __byte_perm(a8, 0u, 0x4342);
 #pragma unroll
