@@ -1257,6 +1257,19 @@ static int plan_build(cs_db* db, int32_t nq, const int32_t* var_off, const int32
       if (c <= 256) nbyte = i + 1;
     }
     d.base = db->cols;
+    if (k >= 4 && k <= CS_MAXK) {
+      // digits in groups of three, each combined in byte lanes when its arity product fits a byte
+      bool ok = true;
+      for (int g0 = 0; g0 < k; g0 += 3) {
+        int64_t gp = 1;
+        for (int i = g0; i < std::min(k, g0 + 3); ++i) {
+          d.gstride[i] = (uint32_t)gp;
+          gp *= db->arity[vars[b + i]];
+        }
+        ok = ok && gp <= 256;
+      }
+      d.g3 = ok ? 1 : 0;
+    }
     const bool sparse = c > ((int64_t)1 << max_dense);
     if (sparse && (flags & F_PARTIAL)) {
       return fail(CS_ERR_UNSUPPORTED, "query %d: sparse (hash) queries cannot be instance-sharded", qbase + q);

@@ -48,6 +48,10 @@ struct __align__(16) QDesc {
   uint32_t R0, R2, P01;
   int32_t npass;                // narrow class: passes over each row segment (cell ranges)
   uint32_t pcells;              // narrow class: cells per pass (multiple of 4)
+  // groups of three digits (0-2, 3-5, 6-7), each combined in byte lanes: set when every group's
+  // arity product is <= 256 (K >= 4); gstride[v] = product of the arities before v in its group
+  int32_t g3;
+  uint32_t gstride[CS_MAXK];
 };
 
 // One unit of work: rows [r0, r1) of query q.

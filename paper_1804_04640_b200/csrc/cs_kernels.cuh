@@ -323,12 +323,55 @@ __device__ __forceinline__ void for_words(const uint32_t (&x)[K][4], WordFn f) {
 
 // Calls run(std::integral_constant<int, NB>) with the compile-time byte-lane digit count the
 // query's nbyte allows: every digit (NB = K), 3, 2, or 0 = decide per digit at run time.
+constexpr int NB_G3 = 103;  // byte-lane split "groups of three digits" (QDesc.g3)
 template <int K, class Run>
-__device__ __forceinline__ void dispatch_nbyte(int nbyte, Run run) {
+__device__ __forceinline__ void dispatch_nbyte(int nbyte, int g3, Run run) {
   if (nbyte >= K) run(std::integral_constant<int, K>{});
+  else if (K > 4 && g3) run(std::integral_constant<int, (K > 4 ? NB_G3 : K)>{});
   else if (K > 3 && nbyte >= 3) run(std::integral_constant<int, (K > 3 ? 3 : K)>{});
   else if (K > 2 && nbyte == 2) run(std::integral_constant<int, (K > 2 ? 2 : K)>{});
   else run(std::integral_constant<int, 0>{});
+}
+
+// Joint index of the 4 rows of one word view in 16-bit lanes (lo = rows 0-1, hi = rows 2-3).
+// NB > 0: digits 0..NB-1 combined in byte lanes (4 rows per IMAD), each later digit split to
+// 16-bit lanes on its own (2 PRMT + 2 IMAD).  NB_G3: digits combined in byte lanes in groups of
+// three (gs = strides inside a group), one split per group (groups of two as the fallback for
+// queries with a triple above 256 measured no gain on cfg5).  NB = 0: per-digit runtime choice.
+template <int K, int NB>
+__device__ __forceinline__ void joint16(const uint32_t (&w)[K], const uint32_t (&st)[K], const uint32_t (&gs)[K],
+                                        int nbyte, uint32_t& lo, uint32_t& hi) {
+  if constexpr (NB == NB_G3) {
+    constexpr int GS = 3, NG = (K + GS - 1) / GS;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      uint32_t g8 = w[GS * g];
+#pragma unroll
+      for (int u = 1; u < GS; ++u)
+        if (GS * g + u < K) g8 += w[GS * g + u] * gs[GS * g + u];
+      if (g == 0) {
+        lo = __byte_perm(g8, 0u, 0x4140);
+        hi = __byte_perm(g8, 0u, 0x4342);
+      } else {
+        lo += __byte_perm(g8, 0u, 0x4140) * st[GS * g];
+        hi += __byte_perm(g8, 0u, 0x4342) * st[GS * g];
+      }
+    }
+  } else {
+    uint32_t a8 = w[0];
+#pragma unroll
+    for (int v = 1; v < K; ++v)
+      if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
+    lo = __byte_perm(a8, 0u, 0x4140);
+    hi = __byte_perm(a8, 0u, 0x4342);
+#pragma unroll
+    for (int v = 1; v < K; ++v) {
+      if (NB ? v >= NB : v >= nbyte) {
+        lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
+        hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
+      }
+    }
+  }
 }
 
 template <int K, int NIB>
@@ -336,11 +379,12 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
                                                  uint32_t* sh) {
   constexpr int RPV = rows_per_vec(NIB);  // rows per 16-byte vector
   const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
-  uint32_t co[K], st[K];
+  uint32_t co[K], st[K], gs[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
     co[v] = q.coff[v];
     st[v] = q.stride[v];
+    gs[v] = q.gstride[v];
   }
   const int nbyte = q.nbyte;
   const int rlog = q.rlog;
@@ -355,11 +399,10 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
   auto run = [&](auto nbc) {
     constexpr int NB = decltype(nbc)::value;
     auto word = [&](const uint32_t (&w)[K]) {
-      uint32_t a8 = w[0];
-#pragma unroll
-      for (int v = 1; v < K; ++v)
-        if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
       if constexpr (NB == K) {
+        uint32_t a8 = w[0];
+#pragma unroll
+        for (int v = 1; v < K; ++v) a8 += w[v] * st[v];
         // every digit in byte lanes (C <= 256): one IDP.4A per row picks the row's byte,
         // scales it by 4R and adds the replica offset -- no split into 16-bit lanes at all
         atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale, rep4)), 1u);
@@ -368,15 +411,8 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
         atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp4a(a8, scale << 24, rep4)), 1u);
         return;
       }
-      uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-      uint32_t hi = __byte_perm(a8, 0u, 0x4342);
-#pragma unroll
-      for (int v = 1; v < K; ++v) {
-        if (NB ? v >= NB : v >= nbyte) {
-          lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
-          hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
-        }
-      }
+      uint32_t lo, hi;
+      joint16<K, NB>(w, st, gs, nbyte, lo, hi);
       // one IDP.2A per row: (16-bit lane) * 4R + 4 * replica, instead of an IMAD per lane pair
       // plus a LOP3 / SHF extract per row on the saturated ALU pipe (4R <= 128 fits the byte)
       atomicAdd(reinterpret_cast<uint32_t*>(shb + __dp2a_lo(lo, scale, rep4)), 1u);
@@ -397,7 +433,7 @@ __device__ __forceinline__ void hist_smem_lane16(const QDesc& q, int64_t r0, int
       }
     }
   };
-  dispatch_nbyte<K>(nbyte, run);
+  dispatch_nbyte<K>(nbyte, q.g3, run);
   const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
   if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(reinterpret_cast<uint32_t*>(shb + rep4), (uint32_t)pad);
@@ -535,11 +571,12 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
                                                  uint32_t* sh) {
   constexpr int RPV = rows_per_vec(NIB);
   const uint8_t* rowp = q.base + (r0 >> row_shift(NIB));
-  uint32_t co[K], st[K];
+  uint32_t co[K], st[K], gs[K];
 #pragma unroll
   for (int v = 0; v < K; ++v) {
     co[v] = q.coff[v];
     st[v] = q.stride[v];
+    gs[v] = q.gstride[v];
   }
   const int nbyte = q.nbyte;
   const int rlog = q.rlog;
@@ -551,19 +588,8 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
   auto run = [&](auto nbc) {
     constexpr int NB = decltype(nbc)::value;  // as in hist_smem_lane16
     auto word = [&](const uint32_t (&w)[K]) {
-      uint32_t a8 = w[0];
-#pragma unroll
-      for (int v = 1; v < K; ++v)
-        if (NB ? v < NB : v < nbyte) a8 += w[v] * st[v];
-      uint32_t lo = __byte_perm(a8, 0u, 0x4140);
-      uint32_t hi = __byte_perm(a8, 0u, 0x4342);
-#pragma unroll
-      for (int v = 1; v < K; ++v) {
-        if (NB ? v >= NB : v >= nbyte) {
-          lo += __byte_perm(w[v], 0u, 0x4140) * st[v];
-          hi += __byte_perm(w[v], 0u, 0x4342) * st[v];
-        }
-      }
+      uint32_t lo, hi;
+      joint16<K, NB>(w, st, gs, nbyte, lo, hi);
       atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(lo, scale, 0u)), 1u);
       atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(lo, scale << 8, 0u)), 1u);
       atomicAdd(reinterpret_cast<uint32_t*>(rbase + __dp2a_lo(hi, scale, 0u)), 1u);
@@ -582,7 +608,7 @@ __device__ __forceinline__ void hist_smem_rows16(const QDesc& q, int64_t r0, int
       }
     }
   };
-  dispatch_nbyte<K>(nbyte, run);
+  dispatch_nbyte<K>(nbyte, q.g3, run);
   const int64_t pad = nvec * RPV - nrows;  // padding rows counted into cell 0
   if (pad > 0 && (int64_t)threadIdx.x == ((nvec - 1) % (int64_t)blockDim.x))
     atomicSub(reinterpret_cast<uint32_t*>(rbase), (uint32_t)pad);
