@@ -1,0 +1,17 @@
+#!/bin/bash
+# round 2 session 6: dot-product row index for two byte-lane groups (k = 5, 6)
+O=gpurun_out/s6g; mkdir -p $O
+one() {  # config label env...
+  c=$1; l=$2; shift; shift
+  env "$@" python bench.py --config $c --no-cpu-baseline --no-dropin 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+print('$c $l', 'dev_ms %.3f'%d['ms_per_step'], 'e2e_ms %.3f'%d['e2e']['ms_per_step'])" | tee -a $O/sweep.txt
+}
+one cfg2 g3 X=1
+one cfg2 dot CS_LIB_PATH=$PWD/tools/libcountgpu_dot.so
+one cfg2 g3 X=1
+one cfg2 dot CS_LIB_PATH=$PWD/tools/libcountgpu_dot.so
+python tools/cfg5_classes.py 2000 "" > $O/classes_g3.txt 2>&1; cat $O/classes_g3.txt
+CS_LIB_PATH=$PWD/tools/libcountgpu_dot.so python tools/cfg5_classes.py 2000 "" > $O/classes_dot.txt 2>&1; cat $O/classes_dot.txt
+CS_LIB_PATH=$PWD/tools/libcountgpu_dot.so timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -m gpu > $O/tests_dot.txt 2>&1; tail -2 $O/tests_dot.txt
