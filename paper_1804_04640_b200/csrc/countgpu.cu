@@ -109,7 +109,7 @@ static const HistFn kHist[CS_MAXK][8][3] = {CS_HK(1), CS_HK(2), CS_HK(3), CS_HK(
 
 // K1r partition kernels per digit count (k >= 2)
 using RadixPartFn = void (*)(const RDesc*, int, int, int64_t, char*);
-using SpillHistFn = void (*)(const SDesc*, const SItem*, int, int*, uint32_t*, char*);
+using SpillHistFn = void (*)(const SDesc*, const SItem*, int, int*, uint32_t*, char*, int);
 static const SpillHistFn kSpillHist[CS_MAXK] = {nullptr,         k_spill_hist<2>, k_spill_hist<3>,
                                                 k_spill_hist<4>, k_spill_hist<5>, k_spill_hist<6>,
                                                 k_spill_hist<7>, k_spill_hist<8>};
@@ -2329,17 +2329,18 @@ extern "C" int cs_plan_execute(cs_plan* p, uint32_t* tables, double* loglik, dou
     const cudaStream_t ss = pick();  // waves share the scratch: one stream for all of them
     CS_CUDA(cudaMemsetAsync(p->d_shead, 0, sizeof(int) * p->sp_heads, ss));
     int hd = 0;
+    const int sp_exact = (flags & F_NARROW_EXACT) ? 1 : 0;  // CS_NARROW_FAST=0: always recount exactly
     for (const auto& wv : p->swaves) {
       for (const auto& L : wv.parts) {
         const int grid = std::min(L.count, ctx->hist_ctas);
         kSpillHist[L.k - 1]<<<grid, SP_THREADS, ctx->hist_smem, ss>>>(p->d_sdesc, p->d_sitems + L.first, L.count,
-                                                                      p->d_shead + hd++, dtab, (char*)scr);
+                                                                      p->d_shead + hd++, dtab, (char*)scr, sp_exact);
         ctx->launches++;
         CS_CUDA(cudaGetLastError());
       }
       const int grid = std::min(wv.nitems, ctx->num_sms);
       k_spill_count<<<grid, SP_THREADS, SP_COUNT_SMEM, ss>>>(p->d_sdesc, p->d_citems + wv.item0, wv.nitems,
-                                                            p->d_shead + hd++, dtab, (const char*)scr);
+                                                            p->d_shead + hd++, dtab, (const char*)scr, sp_exact);
       ctx->launches++;
       CS_CUDA(cudaGetLastError());
     }

@@ -78,6 +78,8 @@ def test_spill_uniform(ctx, monkeypatch, capfd, m):
     assert cls["spill"] == 13 and cls["partition"] == 1
     monkeypatch.setenv("CS_STREAMS", "1")             # every launch on the context stream
     _check(gdb, data, AR, QS)
+    monkeypatch.setenv("CS_NARROW_FAST", "0")         # optimistic passes always followed by the exact recount
+    _check(gdb, data, AR, QS)
 
 
 @pytest.mark.parametrize("slack", ["0", "50", "125"])
