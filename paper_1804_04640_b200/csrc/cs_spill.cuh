@@ -108,7 +108,7 @@ __device__ __forceinline__ void spill_rows(const uint32_t (&x)[K][4], const uint
     for (int h = 0; h < 2; ++h) {
       uint32_t idx[4];
       nib_joint4<K>(x, j, h, rp, R0, R2, P01, idx);
-      if (MODE == 2) {
+      if constexpr (MODE == 2) {
         // all atomics issued before any wrap test reads a result
         uint32_t old[4], inc[4];
 #pragma unroll
@@ -121,37 +121,37 @@ __device__ __forceinline__ void spill_rows(const uint32_t (&x)[K][4], const uint
           for (int t = 0; t < 4; ++t)
             if (byte_wrapped(old[t], inc[t])) narrow_fix<8>(old[t], idx[t] & 3u, idx[t] & ~3u, C, gtab);
         }
-        continue;
-      }
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) reds_byte(tab, idx[t], live && idx[t] < T1);
-      // the other rows: appended to the warp's stream (or, MODE 1, sent to the table one by one)
+        for (int t = 0; t < 4; ++t) reds_byte(tab, idx[t], live && idx[t] < T1);
+        // the other rows: appended to the warp's stream (or, MODE 1, sent to the table one by one)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const bool out = live && idx[t] >= T1;
-        if (MODE == 1) {
-          if (out) {
-            atomicAdd(gtab + idx[t], 1u);
-            ++slow;
+        for (int t = 0; t < 4; ++t) {
+          const bool out = live && idx[t] >= T1;
+          if (MODE == 1) {
+            if (out) {
+              atomicAdd(gtab + idx[t], 1u);
+              ++slow;
+            }
+          } else {
+            // rank among the warp's spilled rows of this slot, one predicated 4-byte store (no
+            // branch), cursor advanced by the slot's count
+            uint32_t n;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t.reg .b32 m, r;\n\t.reg .b64 a;\n\t"
+                "setp.ne.u32 p, %4, 0;\n\t"
+                "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+                "and.b32 r, m, %3;\n\t"
+                "popc.b32 r, r;\n\t"
+                "add.u32 r, r, %2;\n\t"
+                "mad.wide.u32 a, r, 4, %1;\n\t"
+                "@p st.global.u32 [a], %5;\n\t"
+                "popc.b32 %0, m;\n\t}"
+                : "=r"(n)
+                : "l"(reg), "r"(cur), "r"(lt), "r"((uint32_t)out), "r"(idx[t])
+                : "memory");
+            cur += n;
           }
-        } else {
-          // rank among the warp's spilled rows of this slot, one predicated 4-byte store (no
-          // branch), cursor advanced by the slot's count
-          uint32_t n;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t.reg .b32 m, r;\n\t.reg .b64 a;\n\t"
-              "setp.ne.u32 p, %4, 0;\n\t"
-              "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
-              "and.b32 r, m, %3;\n\t"
-              "popc.b32 r, r;\n\t"
-              "add.u32 r, r, %2;\n\t"
-              "mad.wide.u32 a, r, 4, %1;\n\t"
-              "@p st.global.u32 [a], %5;\n\t"
-              "popc.b32 %0, m;\n\t}"
-              : "=r"(n)
-              : "l"(reg), "r"(cur), "r"(lt), "r"((uint32_t)out), "r"(idx[t])
-              : "memory");
-          cur += n;
         }
       }
     }
@@ -318,14 +318,15 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
             if (MODE == 1) mine += on;
           }
         }
-        if (MODE != 2) continue;
-        bool wrap = false;
+        if constexpr (MODE == 2) {
+          bool wrap = false;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) wrap |= byte_wrapped(old[e], inc[e]);
-        if (wrap) {
+          for (int e = 0; e < 8; ++e) wrap |= byte_wrapped(old[e], inc[e]);
+          if (wrap) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (byte_wrapped(old[e], inc[e])) narrow_fix<8>(old[e], c[e] & 3u, c[e] & ~3u, ncell, gt);
+            for (int e = 0; e < 8; ++e)
+              if (byte_wrapped(old[e], inc[e])) narrow_fix<8>(old[e], c[e] & 3u, c[e] & ~3u, ncell, gt);
+          }
         }
       }
     };
