@@ -12,7 +12,8 @@ Other configs (--config cfg1|cfg3|cfg4|cfg5) measure the remaining BASELINE work
 Multi-GPU (torchrun, one rank per GPU, NCCL):
   cfg1-cfg4  query sharding: each rank runs its own slice of an N x batch (weak scaling).
   cfg5       instance sharding: rank g holds rows [g m/N, (g+1) m/N); partial N_ijk tables
-             are summed with an NCCL all-reduce, then LL + MI are scored (strong scaling).
+             are reduce-scattered to their owners over NCCL (CS_BENCH_MERGE=allreduce: summed
+             on every rank), owners score LL + MI, scores all-gathered (strong scaling).
 
 value      units/s over all ranks, device-timed (CUDA events on the launch stream, max over
            ranks), database + plan resident in HBM; L2 flushed (256 MB write) before every
@@ -299,7 +300,7 @@ class QueryRunner:
         self.w, self.queries = workload(args.config, world, rank, args.nq)
         w = self.w
         if args.config == "cfg5":
-            self.kernel = "k_hist + k_radix_part + k_radix_count (histogram phase)"
+            self.kernel = "k_hist + k_spill_hist + k_spill_count + k_radix_part + k_radix_count (histogram phase)"
         # CS_BENCH_FORCE_SHARDED=1 runs the instance-sharded path (CS_PARTIAL + NCCL all-reduce
         # + cs_plan_score) even at world size 1 -- exercises it on a single-GPU box
         self.sharded = args.config == "cfg5" and (world > 1 or os.environ.get("CS_BENCH_FORCE_SHARDED") == "1")
